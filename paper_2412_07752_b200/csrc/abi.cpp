@@ -1,0 +1,303 @@
+// abi.cpp -- the C ABI (include/flashrnn.h): argument validation mirroring the
+// reference's std::invalid_argument checks, the mutex-guarded plan cache, and
+// dispatch to the CUDA kernels.  No CPU fallback: every compute call runs on
+// an sm_100 device or returns an error.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "../../include/flashrnn.h"
+#include "kernels.h"
+#include "planner.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FRNN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// cell.hpp:25-53
+frnn_cell spec_of(int v) {
+  frnn_cell c{};
+  c.variant = v;
+  for (int j = 0; j < 4; ++j) c.uses_recurrent[j] = c.uses_input[j] = 1;
+  switch (v) {
+    case FRNN_ELMAN: c.num_states = 1; c.num_gates = 1; break;
+    case FRNN_LSTM: c.num_states = 2; c.num_gates = 4; break;
+    case FRNN_GRU:
+      c.num_states = 1; c.num_gates = 4;
+      c.uses_recurrent[2] = 0;
+      c.uses_input[3] = 0;
+      break;
+    default: c.num_states = 4; c.num_gates = 4; break;
+  }
+  return c;
+}
+
+// Shape checks of engine.hpp:116-129 (counts, dims, degenerate shape).  The
+// storage-size check is implicit: the ABI takes raw pointers sized by shape.
+int validate(const frnn_cell* cell, const frnn_shape& s, int dtype) {
+  if (!cell) return fail(FRNN_EINVAL_ARG, "null cell");
+  if (cell->variant < FRNN_ELMAN || cell->variant > FRNN_SLSTM)
+    return fail(FRNN_EINVAL_SHAPE, "unknown cell variant");
+  frnn_cell ref = spec_of(cell->variant);
+  if (cell->num_states != ref.num_states || cell->num_gates != ref.num_gates)
+    return fail(FRNN_EINVAL_SHAPE, "cell/params/batch gate or state counts disagree");
+  if (s.head_dim < 1 || s.seq_len < 0 || s.batch < 1 || s.num_heads < 1)
+    return fail(FRNN_EINVAL_SHAPE, "degenerate shape");
+  if (dtype != FRNN_F32 && dtype != FRNN_BF16) return fail(FRNN_EUNSUPPORTED, "unsupported dtype");
+  return FRNN_OK;
+}
+
+int check_device() {
+  static std::once_flag once;
+  static int status = FRNN_OK;
+  static std::string msg;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    cudaDeviceProp prop{};
+    if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) {
+      status = FRNN_ECUDA;
+      msg = std::string("no CUDA device: ") + cudaGetErrorString(e);
+    } else if (prop.major != 10) {
+      status = FRNN_ECUDA;
+      msg = "libflashrnn is built for sm_100a (B200); found sm_" + std::to_string(prop.major * 10 + prop.minor);
+    }
+  });
+  if (status != FRNN_OK) return fail(status, msg);
+  return FRNN_OK;
+}
+
+frnn::Problem make_problem(const frnn_cell* c, const frnn_shape& s, int dtype) {
+  frnn::Problem p{};
+  p.variant = c->variant;
+  p.NS = c->num_states;
+  p.NG = c->num_gates;
+  for (int j = 0; j < 4; ++j) {
+    p.rec[j] = j < p.NG && c->uses_recurrent[j];
+    p.inp[j] = j < p.NG && c->uses_input[j];
+  }
+  p.T = s.seq_len;
+  p.B = s.batch;
+  p.NH = s.num_heads;
+  p.DH = s.head_dim;
+  p.D = s.num_heads * s.head_dim;
+  p.bf16 = dtype == FRNN_BF16;
+  return p;
+}
+
+// ---------------------------------------------------------- plan cache ----
+using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int, int>;
+std::mutex g_mu;
+std::map<Key, frnn::Plan> g_cache;
+
+int get_plan(const frnn::Problem& p, int pass, const frnn_options* o, frnn::Plan* out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int recm = 0, inm = 0;
+  for (int j = 0; j < 4; ++j) {
+    recm |= p.rec[j] << j;
+    inm |= p.inp[j] << j;
+  }
+  const int algo = o ? o->algo : FRNN_ALGO_AUTO;
+  Key k{p.variant, recm, inm, p.T, p.B, p.NH, p.DH, (int)p.bf16, pass, algo, dev, 0};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(k);
+    if (it != g_cache.end()) {
+      *out = it->second;
+      return FRNN_OK;
+    }
+  }
+  std::string why;
+  auto t0 = std::chrono::steady_clock::now();
+  int rc = frnn::solve_plan(p, pass, algo, frnn::device_limits(), out, &why);
+  out->solve_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  if (rc != FRNN_OK) return fail(rc, why);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_cache[k] = *out;
+  return FRNN_OK;
+}
+
+size_t elem(const frnn::Problem& p) { return p.bf16 ? 2 : 4; }
+
+}  // namespace
+
+extern "C" {
+
+const char* frnn_version(void) { return "flashrnn-b200 0.1.0 (sm_100a, abi 1)"; }
+
+const char* frnn_last_error(void) { return g_err.c_str(); }
+
+int frnn_cell_spec(int32_t variant, frnn_cell* out) {
+  if (!out) return fail(FRNN_EINVAL_ARG, "null output");
+  if (variant < FRNN_ELMAN || variant > FRNN_SLSTM) return fail(FRNN_EINVAL_SHAPE, "unknown cell variant");
+  *out = spec_of(variant);
+  return FRNN_OK;
+}
+
+int frnn_plan(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass, const frnn_options* opts,
+              frnn_plan_info* out) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if (!out) return fail(FRNN_EINVAL_ARG, "null output");
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, pass, opts, &pl))) return rc;
+  out->algo = pl.algo;
+  out->rows_per_cta = pl.rows_per_cta;
+  out->batch_tile = pl.batch_tile;
+  out->ctas_per_group = pl.ctas_per_group;
+  out->groups = pl.groups;
+  out->grid = pl.grid;
+  out->threads = pl.threads;
+  out->smem_bytes = pl.smem_bytes;
+  out->tmem_cols = pl.tmem_cols;
+  out->k_split = pl.k_split;
+  out->workspace_bytes = (int64_t)pl.ws_bytes;
+  out->solve_us = pl.solve_us;
+  return FRNN_OK;
+}
+
+int frnn_workspace_size(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                        const frnn_options* opts, size_t* bytes) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if (!bytes) return fail(FRNN_EINVAL_ARG, "null output");
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, pass, opts, &pl))) return rc;
+  *bytes = pl.ws_bytes + 256;  // + the non-finite flag
+  return FRNN_OK;
+}
+
+int frnn_forward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const void* R, const void* bias,
+                 const void* x, const void* s0, void* states, void* gates, void* workspace, size_t ws_bytes,
+                 const frnn_options* opts, void* stream) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if (!R || !bias || !s0 || !states || (shape.seq_len > 0 && (!x || !gates)))
+    return fail(FRNN_EINVAL_ARG, "null tensor pointer");
+  if ((rc = check_device())) return rc;
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  p.R = R; p.bias = bias; p.x = x; p.s0 = s0; p.states = states; p.gates = gates;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t nstate = (size_t)p.NS * p.B * p.D;
+  frnn::Plan pl{};
+  if (p.T > 0 && (rc = get_plan(p, FRNN_PASS_FORWARD, opts, &pl))) return rc;
+  const size_t need = (p.T > 0 ? pl.ws_bytes : 0) + 256;
+  if (!workspace || ws_bytes < need)
+    return fail(FRNN_EINVAL_ARG, "workspace too small: need " + std::to_string(need) + " bytes");
+  cudaError_t e;
+  if (opts && (opts->flags & FRNN_FLAG_CHECK_FINITE)) {  // engine.hpp:146-147
+    int* flag = reinterpret_cast<int*>(static_cast<char*>(workspace) + need - 256);
+    int h = 0;
+    if ((e = cudaMemsetAsync(flag, 0, sizeof(int), s)) != cudaSuccess) return cuda_fail(e, "memset");
+    if ((e = frnn::check_finite(x, (size_t)p.T * p.B * p.NG * p.D, p.bf16, flag, s))) return cuda_fail(e, "finite");
+    if ((e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s))) return cuda_fail(e, "finite");
+    if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "finite");
+    if (h) return fail(FRNN_ENONFINITE, "non-finite input");
+    if ((e = frnn::check_finite(s0, nstate, p.bf16, flag, s))) return cuda_fail(e, "finite");
+    if ((e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s))) return cuda_fail(e, "finite");
+    if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "finite");
+    if (h) return fail(FRNN_ENONFINITE, "non-finite initial state");
+  }
+  if (p.T == 0) {  // states = [s0]
+    if ((e = cudaMemcpyAsync(states, s0, nstate * elem(p), cudaMemcpyDeviceToDevice, s)))
+      return cuda_fail(e, "copy s0");
+    return FRNN_OK;
+  }
+  switch (pl.algo) {
+    case FRNN_ALGO_SIMT: e = frnn::simt_forward(p, pl, workspace, s); break;
+    case FRNN_ALGO_FUSED: e = frnn::fused_forward(p, pl, workspace, s); break;
+    default: e = frnn::alt_forward(p, pl, workspace, s); break;
+  }
+  if (e == cudaErrorNotSupported) return fail(FRNN_EUNSUPPORTED, "algorithm not implemented for this shape");
+  if (e != cudaSuccess) return cuda_fail(e, "forward launch");
+  return FRNN_OK;
+}
+
+int frnn_backward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const void* R, const void* bias,
+                  const void* states, const void* gates, const void* d_states_final, const void* d_hidden,
+                  frnn_clip clip, void* dx, void* dbias, void* dR, void* ds0, void* workspace, size_t ws_bytes,
+                  const frnn_options* opts, void* stream) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if (clip.mode == FRNN_CLIP_VALUE && !(clip.magnitude > 0))  // engine.hpp:107
+    return fail(FRNN_EINVAL_ARG, "clip magnitude must be positive");
+  if (clip.mode < FRNN_CLIP_OFF || clip.mode > FRNN_CLIP_ZERO) return fail(FRNN_EINVAL_ARG, "bad clip mode");
+  if (!R || !states || !d_states_final || !dbias || !dR || !ds0 || (shape.seq_len > 0 && (!gates || !dx)))
+    return fail(FRNN_EINVAL_ARG, "null tensor pointer");
+  if ((rc = check_device())) return rc;
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  p.R = R; p.bias = bias; p.cstates = states; p.cgates = gates; p.dsf = d_states_final; p.dh = d_hidden;
+  p.clip_mode = clip.mode;
+  p.clip_mag = (float)clip.magnitude;
+  p.dx = dx; p.dbias = dbias; p.dR = dR; p.ds0 = ds0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (p.T == 0) {  // no steps: ds0 = d_states_final, zero parameter grads
+    const size_t nstate = (size_t)p.NS * p.B * p.D;
+    if ((e = cudaMemcpyAsync(ds0, d_states_final, nstate * elem(p), cudaMemcpyDeviceToDevice, s)) ||
+        (e = cudaMemsetAsync(dbias, 0, (size_t)p.NG * p.D * elem(p), s)) ||
+        (e = cudaMemsetAsync(dR, 0, (size_t)p.NH * p.NG * p.DH * p.DH * elem(p), s)))
+      return cuda_fail(e, "T=0 backward");
+    return FRNN_OK;
+  }
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, FRNN_PASS_BACKWARD, opts, &pl))) return rc;
+  const size_t need = pl.ws_bytes + 256;
+  if (!workspace || ws_bytes < need)
+    return fail(FRNN_EINVAL_ARG, "workspace too small: need " + std::to_string(need) + " bytes");
+  switch (pl.algo) {
+    case FRNN_ALGO_SIMT: e = frnn::simt_backward(p, pl, workspace, s); break;
+    case FRNN_ALGO_FUSED: e = frnn::fused_backward(p, pl, workspace, s); break;
+    default: e = frnn::alt_backward(p, pl, workspace, s); break;
+  }
+  if (e == cudaErrorNotSupported) return fail(FRNN_EUNSUPPORTED, "algorithm not implemented for this shape");
+  if (e != cudaSuccess) return cuda_fail(e, "backward launch");
+  return FRNN_OK;
+}
+
+// Batch x head sharding over world_size ranks: heads split by the
+// largest factor of world_size dividing NH; the rest of world_size splits B.
+int frnn_partition(frnn_shape shape, int32_t world_size, int32_t rank, frnn_shard* out) {
+  g_err.clear();
+  if (!out) return fail(FRNN_EINVAL_ARG, "null output");
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(FRNN_EINVAL_ARG, "bad rank/world size");
+  if (shape.batch < 1 || shape.num_heads < 1) return fail(FRNN_EINVAL_SHAPE, "degenerate shape");
+  int hs = 1;
+  for (int f = 1; f <= world_size; ++f)
+    if (world_size % f == 0 && shape.num_heads % f == 0) hs = f;
+  int bs = world_size / hs;
+  if (bs > shape.batch) return fail(FRNN_EINVAL_SHAPE, "more batch shards than batch rows");
+  const int hp = rank / bs, bp = rank % bs;
+  const int hper = shape.num_heads / hs;
+  out->head_begin = hp * hper;
+  out->head_end = (hp + 1) * hper;
+  out->batch_begin = (int)((long long)shape.batch * bp / bs);
+  out->batch_end = (int)((long long)shape.batch * (bp + 1) / bs);
+  out->reduce_params = bs > 1;
+  return FRNN_OK;
+}
+
+}  // extern "C"

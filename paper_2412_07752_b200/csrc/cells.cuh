@@ -1,0 +1,204 @@
+// cells.cuh -- device-side cell functors (Elman / LSTM / GRU / sLSTM).
+//
+// Restates rnnkit's pointwise maps on the device:
+//   forward:  cell.hpp:65-99   (pointwise_forward)
+//   backward: cell.hpp:108-201 (pointwise_jacobians) contracted with the state
+//             gradient exactly as engine.hpp:275-284 does:
+//             dg[j] = sum_i J.d_gate[i][j] * ds[i],  dsp[k] = sum_i J.d_prev[i][k] * ds[i]
+// Numerics follow scalar.hpp:58-76: sigma(x) = 1/(1+e^-x), log-sigma split at 0
+// with log1p, max_(a,b) = a > b ? a : b, and the sLSTM tie rule of cell.hpp:153
+// (ties go to the forget branch in the Jacobian).
+//
+// Math<false> uses IEEE-accurate libdevice functions (fp32 parity mode, rel 1e-5);
+// Math<true> uses the MUFU approximations (bf16 mode, whose tolerance is 2e-2).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace frnn {
+
+enum Variant { kElman = 0, kLstm = 1, kGru = 2, kSlstm = 3 };
+
+template <bool FAST>
+struct Math {
+  static __device__ __forceinline__ float ex(float x) { return FAST ? __expf(x) : expf(x); }
+  static __device__ __forceinline__ float th(float x) {
+    if (FAST) {
+      float y;
+      asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+      return y;
+    }
+    return tanhf(x);
+  }
+  static __device__ __forceinline__ float l1p(float x) { return FAST ? __logf(1.0f + x) : log1pf(x); }
+  static __device__ __forceinline__ float sig(float x) {
+    return FAST ? __fdividef(1.0f, 1.0f + __expf(-x)) : 1.0f / (1.0f + expf(-x));
+  }
+  static __device__ __forceinline__ float logsig(float x) {  // scalar.hpp:64-70
+    return x >= 0.f ? -l1p(ex(-x)) : x - l1p(ex(x));
+  }
+  static __device__ __forceinline__ float rcp(float x) { return FAST ? __fdividef(1.0f, x) : 1.0f / x; }
+};
+
+// Compile-time cell traits.  NGP = gate rows per hidden unit in the tensor-core
+// tiles (all NG gates, padded to a power of two).
+template <int V>
+struct Cell;
+
+template <>
+struct Cell<kElman> {
+  static constexpr int NS = 1, NG = 1, NGP = 1;
+  static constexpr bool rec(int) { return true; }
+  static constexpr bool inp(int) { return true; }
+  template <class M>
+  static __device__ __forceinline__ void fwd(const float* p, const float* g, float* n) {
+    n[0] = M::th(g[0]);  // cell.hpp:69-72
+  }
+  template <class M>
+  static __device__ __forceinline__ void bwd(const float* p, const float* g, const float* ds,
+                                             float* dg, float* dsp) {
+    float t = M::th(g[0]);
+    dg[0] = (1.f - t * t) * ds[0];  // cell.hpp:114-117
+    dsp[0] = 0.f;
+  }
+};
+
+template <>
+struct Cell<kLstm> {
+  static constexpr int NS = 2, NG = 4, NGP = 4;
+  static constexpr bool rec(int) { return true; }
+  static constexpr bool inp(int) { return true; }
+  template <class M>
+  static __device__ __forceinline__ void fwd(const float* p, const float* g, float* n) {
+    // cell.hpp:73-78
+    float c = M::sig(g[1]) * p[1] + M::sig(g[2]) * M::th(g[0]);
+    n[0] = M::sig(g[3]) * M::th(c);
+    n[1] = c;
+  }
+  template <class M>
+  static __device__ __forceinline__ void bwd(const float* p, const float* g, const float* ds,
+                                             float* dg, float* dsp) {
+    // cell.hpp:119-135
+    float sf = M::sig(g[1]), si = M::sig(g[2]), so = M::sig(g[3]);
+    float tz = M::th(g[0]);
+    float c = sf * p[1] + si * tz;
+    float tc = M::th(c);
+    float dtc = 1.f - tc * tc;
+    float J10 = si * (1.f - tz * tz);
+    float J11 = sf * (1.f - sf) * p[1];
+    float J12 = si * (1.f - si) * tz;
+    float P11 = sf;
+    float J00 = so * dtc * J10, J01 = so * dtc * J11, J02 = so * dtc * J12;
+    float J03 = so * (1.f - so) * tc;
+    float P01 = so * dtc * sf;
+    dg[0] = J00 * ds[0] + J10 * ds[1];
+    dg[1] = J01 * ds[0] + J11 * ds[1];
+    dg[2] = J02 * ds[0] + J12 * ds[1];
+    dg[3] = J03 * ds[0];
+    dsp[0] = 0.f;
+    dsp[1] = P01 * ds[0] + P11 * ds[1];
+  }
+};
+
+template <>
+struct Cell<kGru> {
+  static constexpr int NS = 1, NG = 4, NGP = 4;
+  static constexpr bool rec(int j) { return j != 2; }  // n skips R   (cell.hpp:43)
+  static constexpr bool inp(int j) { return j != 3; }  // g skips x   (cell.hpp:44)
+  template <class M>
+  static __device__ __forceinline__ void fwd(const float* p, const float* g, float* n) {
+    // cell.hpp:79-84
+    float sz = M::sig(g[0]);
+    float inner = g[2] + M::sig(g[1]) * M::th(g[3]);
+    n[0] = sz * p[0] + (1.f - sz) * M::th(inner);
+  }
+  template <class M>
+  static __device__ __forceinline__ void bwd(const float* p, const float* g, const float* ds,
+                                             float* dg, float* dsp) {
+    // cell.hpp:136-149
+    float sz = M::sig(g[0]), sr = M::sig(g[1]);
+    float tg = M::th(g[3]);
+    float u = g[2] + sr * tg;
+    float tu = M::th(u);
+    float dtu = 1.f - tu * tu;
+    float omz = 1.f - sz;
+    dg[0] = sz * (1.f - sz) * (p[0] - tu) * ds[0];
+    dg[1] = omz * dtu * sr * (1.f - sr) * tg * ds[0];
+    dg[2] = omz * dtu * ds[0];
+    dg[3] = omz * dtu * sr * (1.f - tg * tg) * ds[0];
+    dsp[0] = sz * ds[0];
+  }
+};
+
+template <>
+struct Cell<kSlstm> {
+  static constexpr int NS = 4, NG = 4, NGP = 4;
+  static constexpr bool rec(int) { return true; }
+  static constexpr bool inp(int) { return true; }
+  template <class M>
+  static __device__ __forceinline__ void fwd(const float* p, const float* g, float* n) {
+    // cell.hpp:85-97
+    float a = M::logsig(g[1]) + p[3];
+    float m = a > g[2] ? a : g[2];
+    float fexp = M::ex(a - m);
+    float iexp = M::ex(g[2] - m);
+    float c = fexp * p[1] + iexp * M::th(g[0]);
+    float nn = fexp * p[2] + iexp;
+    n[0] = M::sig(g[3]) * (c * M::rcp(nn));
+    n[1] = c;
+    n[2] = nn;
+    n[3] = m;
+  }
+  template <class M>
+  static __device__ __forceinline__ void bwd(const float* p, const float* g, const float* ds,
+                                             float* dg, float* dsp) {
+    // cell.hpp:150-198
+    float sf = M::sig(g[1]), so = M::sig(g[3]);
+    float a = M::logsig(g[1]) + p[3];
+    bool use_a = !(a < g[2]);  // ties -> forget branch (cell.hpp:153)
+    float m = use_a ? a : g[2];
+    float fexp = M::ex(a - m);
+    float iexp = M::ex(g[2] - m);
+    float tz = M::th(g[0]);
+    float c = fexp * p[1] + iexp * tz;
+    float n = fexp * p[2] + iexp;
+    float da_df = 1.f - sf;
+    float dm_df = use_a ? da_df : 0.f;
+    float dm_di = use_a ? 0.f : 1.f;
+    float dm_dmp = use_a ? 1.f : 0.f;
+    float dfexp_df = fexp * (da_df - dm_df);
+    float diexp_df = -iexp * dm_df;
+    float dfexp_di = -fexp * dm_di;
+    float diexp_di = iexp * (1.f - dm_di);
+    float dfexp_dmp = fexp * (1.f - dm_dmp);
+    float diexp_dmp = -iexp * dm_dmp;
+    float J10 = iexp * (1.f - tz * tz);
+    float J11 = dfexp_df * p[1] + diexp_df * tz;
+    float J12 = dfexp_di * p[1] + diexp_di * tz;
+    float P11 = fexp;
+    float P13 = dfexp_dmp * p[1] + diexp_dmp * tz;
+    float J21 = dfexp_df * p[2] + diexp_df;
+    float J22 = dfexp_di * p[2] + diexp_di;
+    float P22 = fexp;
+    float P23 = dfexp_dmp * p[2] + diexp_dmp;
+    float J31 = dm_df, J32 = dm_di, P33 = dm_dmp;
+    float inv_n = M::rcp(n);
+    float h_over = c * inv_n;
+    float J00 = so * J10 * inv_n;                      // J20 = 0
+    float J01 = so * (J11 - h_over * J21) * inv_n;
+    float J02 = so * (J12 - h_over * J22) * inv_n;
+    float J03 = so * (1.f - so) * h_over;               // J13 = J23 = 0
+    float P01 = so * P11 * inv_n;                       // P21 = 0
+    float P02 = so * (-h_over * P22) * inv_n;           // P12 = 0
+    float P03 = so * (P13 - h_over * P23) * inv_n;
+    dg[0] = J00 * ds[0] + J10 * ds[1];
+    dg[1] = J01 * ds[0] + J11 * ds[1] + J21 * ds[2] + J31 * ds[3];
+    dg[2] = J02 * ds[0] + J12 * ds[1] + J22 * ds[2] + J32 * ds[3];
+    dg[3] = J03 * ds[0];
+    dsp[0] = 0.f;
+    dsp[1] = P01 * ds[0] + P11 * ds[1];
+    dsp[2] = P02 * ds[0] + P22 * ds[2];
+    dsp[3] = P03 * ds[0] + P13 * ds[1] + P23 * ds[2] + P33 * ds[3];
+  }
+};
+
+}  // namespace frnn

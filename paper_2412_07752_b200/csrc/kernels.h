@@ -1,0 +1,75 @@
+// kernels.h -- internal launch interface between the C-ABI layer (abi.cpp) and
+// the CUDA translation units.  Not installed; the public surface is flashrnn.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace frnn {
+
+// Everything a pass needs, device pointers only.  Element type is given by
+// `bf16` (true: __nv_bfloat16, false: float).
+struct Problem {
+  int variant, NS, NG;
+  bool rec[4], inp[4];
+  int T, B, NH, DH, D;
+  bool bf16;
+  // forward
+  const void *R, *bias, *x, *s0;
+  void *states, *gates;
+  // backward
+  const void *cstates, *cgates, *dsf, *dh;
+  int clip_mode;
+  float clip_mag;
+  void *dx, *dbias, *dR, *ds0;
+};
+
+// Tiling chosen by the planner for one pass.
+struct Plan {
+  int algo;            // frnn_algo
+  int rows_per_cta;    // tcgen05 M (128) or SIMT rows
+  int batch_tile;      // N
+  int units_per_cta;   // hidden units owned per CTA
+  int ctas_per_group;  // CTAs synchronising per step
+  int groups;          // heads x batch tiles
+  int grid, threads, smem_bytes, tmem_cols, k_split;
+  size_t ws_bytes;
+  double solve_us;
+};
+
+// Workspace carve-up helpers.
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---- SIMT fp32 path (simt_fp32.cu) ----
+size_t simt_smem_bytes(const Problem& p, bool backward);
+cudaError_t simt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+cudaError_t simt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+
+// ---- fused tcgen05 bf16 path (fused_bf16.cu) ----
+cudaError_t fused_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+cudaError_t fused_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+size_t fused_forward_ws(const Problem& p, const Plan& pl);
+size_t fused_backward_ws(const Problem& p, const Plan& pl);
+
+// ---- alternating path (alternating.cu) ----
+cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+size_t alt_forward_ws(const Problem& p, const Plan& pl);
+size_t alt_backward_ws(const Problem& p, const Plan& pl);
+
+// ---- parameter gradients dR / db (param_grads.cu) ----
+// dg element (t, b, j, e) lives at dg[t*ts + b*bs + j*js + e].
+struct DgView {
+  const void* ptr;
+  long long ts, bs, js;
+};
+cudaError_t param_grads(const Problem& p, DgView dg, void* ws, cudaStream_t s);
+size_t param_grads_ws(const Problem& p);
+
+// ---- utilities (util.cu) ----
+// Sets *flag (device int) to 1 if any of the n elements is non-finite.
+cudaError_t check_finite(const void* ptr, size_t n, bool bf16, int* flag, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace frnn

@@ -1,0 +1,29 @@
+// planner.h -- B200 tiling solver interface (ConstrINT-style integer CSP; see
+// planner.cpp and DESIGN.md section 5).
+#pragma once
+#include <string>
+
+#include "kernels.h"
+
+namespace frnn {
+
+// Hardware limits the constraints are built from (queried from the device,
+// B200 defaults when none is present).
+struct DeviceLimits {
+  int sm_count = 148;
+  int smem_optin = 232448;        // max dynamic shared memory per CTA (bytes)
+  int regs_per_sm = 65536;        // 32-bit registers
+  int tmem_cols = 512;            // TMEM columns (x 128 lanes x 32 bit) per SM
+  int max_threads = 1024;
+  int cluster_max = 8;
+  int umma_m = 128;               // tcgen05 kind::f16 M with cta_group::1
+  int umma_k = 16;                // tcgen05 kind::f16 K per instruction
+};
+const DeviceLimits& device_limits();
+
+// Fills *out for the pass (0 fwd, 1 bwd).  algo_request is an frnn_algo.
+// Returns an frnn_status; *why explains infeasibility.
+int solve_plan(const Problem& p, int pass, int algo_request, const DeviceLimits& lim, Plan* out,
+               std::string* why);
+
+}  // namespace frnn

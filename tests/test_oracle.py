@@ -1,0 +1,188 @@
+"""CPU tests of the parity oracle (oracle/rnn_oracle.c).
+
+The oracle is pinned two ways: bit-exact against the golden vectors the
+unmodified reference engine produced (tests/golden/, make_golden.py), and
+bit-exact against the reference compiled in place (oracle/_ref) on fresh
+seeds.  The SPEC known-answer tests then check the oracle's
+semantics directly.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import normwise
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+VARIANTS = ["elman", "lstm", "gru", "slstm"]
+
+
+def _golden(v):
+    return dict(np.load(os.path.join(GOLDEN, f"{v}_small.npz")))
+
+
+def test_golden_files_present():
+    assert len(glob.glob(os.path.join(GOLDEN, "*_small.npz"))) == 4
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+def test_oracle_matches_golden_bitexact(orc, v):
+    g = _golden(v)
+    T, B, NH, DH = g["shape"]
+    gen = orc.generate(v, int(T), int(B), int(NH), int(DH), seed=11 + VARIANTS.index(v))
+    for k in ("R", "bias", "x", "s0", "dsf"):
+        assert np.array_equal(gen[k], g[k]), k  # reference generator reproduced bit-exactly
+    for dt, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        st, ga = orc.forward(v, g["R"], g["bias"], g["x"], g["s0"], dtype=dt)
+        assert np.array_equal(st, g[f"{tag}_states"])
+        assert np.array_equal(ga, g[f"{tag}_gates"])
+        for clip, mag, dh in (("off", 0.0, None), ("value", 0.05, None), ("zero", 0.0, None),
+                              ("off", 0.0, g["d_hidden"])):
+            key = f"{tag}_{clip}" + ("_dh" if dh is not None else "")
+            out = orc.backward(v, g["R"], st, ga, g["dsf"], clip, mag, dh, dtype=dt)
+            for name, arr in out.items():
+                assert np.array_equal(arr, g[f"{key}_{name}"]), (key, name)
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+@pytest.mark.parametrize("seed", [0, 5])
+def test_oracle_matches_reference_bitexact(orc, ref, v, seed):
+    T, B, NH, DH = 5, 3, 3, 8
+    a = ref.generate(v, T, B, NH, DH, seed)
+    s1, g1 = orc.forward(v, a["R"], a["bias"], a["x"], a["s0"])
+    s2, g2 = ref.forward(v, a["R"], a["bias"], a["x"], a["s0"])
+    assert np.array_equal(s1, s2) and np.array_equal(g1, g2)
+    dh = np.random.RandomState(seed).randn(T, B, NH * DH)
+    o1 = orc.backward(v, a["R"], s1, g1, a["dsf"], "value", 0.3, dh)
+    o2 = ref.backward(v, a["R"], a["bias"], a["x"], a["s0"], s2, g2, a["dsf"], "value", 0.3, dh)
+    for k in o1:
+        assert np.array_equal(o1[k], o2[k]), k
+
+
+# ---------------------------------------------------------------- SPEC KATs --
+def test_lstm_zero_fixed_point(orc):
+    T, B, NH, DH = 6, 2, 1, 4
+    z = lambda *s: np.zeros(s)
+    st, ga = orc.forward("lstm", z(NH, 4, DH, DH), z(4, DH), z(T, B, 4, DH), z(2, B, DH))
+    assert np.all(st == 0) and np.all(ga == 0)
+
+
+def test_lstm_c_halves(orc):  # zero params, c0 = 1, x = 0 -> c_t = 0.5^t
+    T, B, NH, DH = 10, 2, 1, 4
+    s0 = np.zeros((2, B, DH))
+    s0[1] = 1.0
+    st, _ = orc.forward("lstm", np.zeros((NH, 4, DH, DH)), np.zeros((4, DH)),
+                        np.zeros((T, B, 4, DH)), s0)
+    for t in range(T + 1):
+        assert np.all(st[t, 1] == 0.5 ** t)
+
+
+def test_slstm_stabilizer_bounds(orc):  # SPEC.md:405, :452 (|g| <= 50 stays finite)
+    rng = np.random.RandomState(0)
+    T, B, NH, DH = 8, 4, 1, 8
+    R = rng.randn(NH, 4, DH, DH) * 3
+    x = rng.uniform(-50, 50, (T, B, 4, DH))
+    s0 = np.zeros((4, B, DH))
+    s0[2] = 1.0
+    st, ga = orc.forward("slstm", R, np.zeros((4, DH)), x, s0)
+    assert np.all(np.isfinite(st))
+    for t in range(T):
+        m_prev, m = st[t, 3], st[t + 1, 3]
+        f, i = ga[t, 1], ga[t, 2]
+        a = np.where(f >= 0, -np.log1p(np.exp(-f)), f - np.log1p(np.exp(f))) + m_prev
+        # recomputed in numpy, so allow last-ulp differences from libm
+        assert np.all(a - m <= 1e-12 * np.maximum(1, np.abs(m))) and np.all(i - m <= 0)
+        assert np.all(st[t + 1, 2] > 0)
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+def test_t1_bias_equals_gate_grad(orc, v):  # T=1 -> db = sum_b dg
+    a = orc.generate(v, 1, 3, 2, 8, seed=1)
+    st, ga = orc.forward(v, a["R"], a["bias"], a["x"], a["s0"])
+    g = orc.backward(v, a["R"], st, ga, a["dsf"])
+    ns, ng, rec, inp = __import__("oracle").cell_spec(v)
+    for j in range(ng):
+        if inp[j]:
+            assert np.array_equal(g["dx"][0, :, j].sum(0), g["dbias"][j]) or np.allclose(
+                g["dx"][0, :, j].sum(0), g["dbias"][j], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+def test_blockdiag_equivalence(ref, v):
+    a = ref.generate(v, 6, 2, 3, 8, seed=2)
+    assert ref.blockdiag_check(v, a["R"], a["bias"], a["x"], a["s0"]) <= 1e-12
+
+
+def test_gru_wiring(orc):  # x never reaches gate g, h never reaches gate n
+    a = orc.generate("gru", 4, 2, 1, 8, seed=3)
+    _, g1 = orc.forward("gru", a["R"], a["bias"], a["x"], a["s0"])
+    x2 = a["x"].copy()
+    x2[:, :, 3] += 7.0
+    _, g2 = orc.forward("gru", a["R"], a["bias"], x2, a["s0"])
+    assert np.array_equal(g1, g2)
+    s2 = a["s0"].copy()
+    s2 += 3.0
+    _, g3 = orc.forward("gru", a["R"], a["bias"], a["x"], s2)
+    assert np.array_equal(g1[0, 2], g3[0, 2])
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+def test_clip_identities(orc, v):
+    a = orc.generate(v, 6, 2, 2, 8, seed=4)
+    st, ga = orc.forward(v, a["R"], a["bias"], a["x"], a["s0"])
+    off = orc.backward(v, a["R"], st, ga, a["dsf"], "off")
+    big = orc.backward(v, a["R"], st, ga, a["dsf"], "value", 1e30)
+    for k in off:
+        assert np.array_equal(off[k], big[k])
+
+
+def test_jacobian_fd(orc):  # Jacobians vs finite differences
+    rng = np.random.RandomState(7)
+    import oracle as O
+    for v in VARIANTS:
+        ns, ng, _, _ = O.cell_spec(v)
+        for _ in range(20):
+            prev = rng.randn(4)
+            prev[2] = abs(prev[2]) + 0.5
+            g = rng.randn(4) * 2
+            Jg, Jp = orc.jacobians(v, prev, g)
+            h = 1e-6
+            for j in range(ng):
+                gp, gm = g.copy(), g.copy()
+                gp[j] += h
+                gm[j] -= h
+                fd = (orc.pointwise(v, prev, gp) - orc.pointwise(v, prev, gm)) / (2 * h)
+                assert np.allclose(fd[:ns], Jg[:ns, j], atol=1e-7, rtol=1e-6), (v, j)
+            for k in range(ns):
+                pp, pm = prev.copy(), prev.copy()
+                pp[k] += h
+                pm[k] -= h
+                fd = (orc.pointwise(v, pp, g) - orc.pointwise(v, pm, g)) / (2 * h)
+                assert np.allclose(fd[:ns], Jp[:ns, k], atol=1e-7, rtol=1e-6), (v, k)
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+def test_reference_gradcheck_sane(ref, v):  # gradcheck.cpp:18-75 with h=1e-5, floor=1e-2
+    r = ref.gradient_check(v, step=1e-5, floor=1e-2)
+    assert np.all(r < 1e-5), r
+
+
+def test_bf16_rounding(orc):
+    x = np.array([1.0, 1.00390625, 1.005859375, -3.14159, 0.0])
+    r = orc.round_bf16(x)
+    assert r[0] == 1.0 and r[1] == 1.0 and r[2] == 1.0078125 and r[4] == 0.0
+    assert abs(r[3] - np.float32(-3.140625)) == 0
+
+
+def test_fp32_engine_within_normwise_tolerance(orc):
+    """Calibrates the fp32 parity metric: the reference's own float engine is
+    within normwise 1e-5 of the double engine at config 1."""
+    a = orc.generate("lstm", 64, 8, 1, 64, seed=0)
+    s64, g64 = orc.forward("lstm", a["R"], a["bias"], a["x"], a["s0"])
+    s32, g32 = orc.forward("lstm", a["R"], a["bias"], a["x"], a["s0"], np.float32)
+    G64 = orc.backward("lstm", a["R"], s64, g64, a["dsf"])
+    G32 = orc.backward("lstm", a["R"], s32, g32, a["dsf"], dtype=np.float32)
+    assert normwise(s32, s64) < 1e-5
+    for k in G64:
+        assert normwise(G32[k], G64[k]) < 1e-5
