@@ -1,0 +1,433 @@
+#!/usr/bin/env python3
+"""bench.py -- FlashRNN-B200 headline benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one forward + backward pass of the recurrence (rnnkit forward +
+backward, engine.hpp:144/:222) over one batch: sLSTM, bf16, B=16 per GPU,
+T=1024, H=768, NH=1 (BASELINE configs[1], the metric's workload), synthetic
+inputs drawn on the device with the reference generator's distributions
+(random_init.hpp:10-40).  Multi-GPU (torchrun, one rank per GPU, NCCL): weak
+scaling -- every rank runs its own B=16 shard (frnn_partition batch sharding)
+with no per-step communication, then dR/db are sum-reduced (the only
+collective) inside the timed step.
+
+value    device time (CUDA events on the launching stream) of K steps with
+         inputs resident in HBM; L2 flushed (256 MB write) between timed steps;
+         max over ranks; B*T*N / s.
+e2e      the same metric through the C ABI with HOST buffers: pinned inputs
+         (R, b, x, s0, dL/ds_T) copied H2D and the parameter gradients + ds0
+         copied D2H inside the timed region, every step.
+roofline the dominant kernel (largest share of the step), timed live with CUDA
+         events on its launch stream (frnn_debug_kernel_ms); algorithmic FLOPs
+         per launch = 2*NG_rec*NH*DH^2*B*T (its contraction); peak = measured
+         sustained bf16 (MEASURED_PEAKS.json).
+cpu_baseline  the unmodified reference engine (oracle/_ref, engine<float>)
+         on this host, batch rows sharded over processes, bounded T sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sLSTM/LSTM fwd+bwd batch·timesteps/sec at B16 T1024 H768, 1/2/4/8 B200"
+UNIT = "batch*timesteps/s"
+NS_NG = {"elman": (1, 1), "lstm": (2, 4), "gru": (1, 4), "slstm": (4, 4)}
+NGREC = {"elman": 1, "lstm": 4, "gru": 3, "slstm": 4}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--variant", default="slstm", choices=list(NS_NG))
+    ap.add_argument("--heads", type=int, default=1)
+    ap.add_argument("--hidden", type=int, default=768)
+    ap.add_argument("--batch", type=int, default=16, help="batch rows per GPU")
+    ap.add_argument("--seq", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=64)
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"{a.variant} fwd+bwd bf16, B={a.batch}/GPU, T={a.seq}, H={a.hidden}, NH={a.heads}"
+            + (" (fused kernel, R resident on-chip)" if a.hidden // a.heads <= 768 else ""))
+
+
+def flops_per_pass(a):
+    """Algorithmic FLOPs of one recurrence contraction pass (fwd R.h, bwd R^T.dg,
+    or dR): 2 * NG_rec * NH * DH^2 per batch-timestep (planner.cpp:404-416)."""
+    dh = a.hidden // a.heads
+    return 2.0 * NGREC[a.variant] * a.heads * dh * dh * a.batch * a.seq
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                               f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(torch, dev, a, seed):
+    """Synthetic inputs with the reference generator's distributions
+    (random_init.hpp:10-40): R ~ N(0, 1/DH), b ~ N(0, 0.1^2), x ~ N(0,1),
+    s0 ~ N(0, 0.5^2) (sLSTM n0 = 1 + 0.1|.|, m0 = 0), dL/ds_T ~ N(0,1)."""
+    ns, ng = NS_NG[a.variant]
+    nh, dh, B, T = a.heads, a.hidden // a.heads, a.batch, a.seq
+    D = nh * dh
+    g = torch.Generator(device=dev).manual_seed(seed)
+    R = (torch.randn(nh, ng, dh, dh, device=dev, generator=g) / dh ** 0.5).bfloat16()
+    b = (0.1 * torch.randn(ng, D, device=dev, generator=g)).bfloat16()
+    x = torch.randn(T, B, ng, D, device=dev, generator=g).bfloat16()
+    s0 = 0.5 * torch.randn(ns, B, D, device=dev, generator=g)
+    if a.variant == "slstm":
+        s0[2] = 1 + 0.1 * s0[2].abs()
+        s0[3] = 0
+    s0 = s0.bfloat16()
+    dsf = torch.randn(ns, B, D, device=dev, generator=g).bfloat16()
+    return dict(R=R, bias=b, x=x, s0=s0, dsf=dsf)
+
+
+# ----------------------------------------------------------- CPU baseline ----
+def _ref_worker(args):
+    """One batch row through the unmodified reference engine<float>."""
+    variant, T, DH, NH, seed = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+    ref = O.Reference()
+    ns, ng = NS_NG[variant]
+    rng = np.random.RandomState(seed)
+    D = NH * DH
+    R = (rng.randn(NH, ng, DH, DH) / DH ** 0.5).astype(np.float32)
+    b = (0.1 * rng.randn(ng, D)).astype(np.float32)
+    x = rng.randn(T, 1, ng, D).astype(np.float32)
+    s0 = (0.5 * rng.randn(ns, 1, D)).astype(np.float32)
+    if variant == "slstm":
+        s0[2] = 1 + 0.1 * np.abs(s0[2])
+        s0[3] = 0
+    dsf = rng.randn(ns, 1, D).astype(np.float32)
+    t0 = time.perf_counter()
+    st, ga = ref.forward(variant, R, b, x, s0, dtype=np.float32)
+    ref.backward(variant, R, b, x, s0, st, ga, dsf, dtype=np.float32)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_step(a, T_sample, pool, cores):
+    """One bounded sample of the workload on the host: the a.batch rows are
+    independent (engine.hpp:173, only dR/db sum over b), so each row is one
+    reference call in its own process; returns (B*T/s, wall seconds)."""
+    jobs = [(a.variant, T_sample, a.hidden // a.heads, a.heads, 1000 + r) for r in range(a.batch)]
+    t0 = time.perf_counter()
+    list(pool.map(_ref_worker, jobs))
+    wall = time.perf_counter() - t0
+    return a.batch * T_sample / wall, wall
+
+
+def make_pool(a):
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    cores = max(1, min(os.cpu_count() or 1, a.batch))
+    return cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork")), cores
+
+
+def cpu_baseline(a):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.Reference.available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libref.so not built"}
+    pool, cores = make_pool(a)
+    try:
+        cpu_reference_step(a, 2, pool, cores)  # warm the workers
+        v, wall = cpu_reference_step(a, a.cpu_sample_steps, pool, cores)
+    finally:
+        pool.shutdown()
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": (f"unmodified rnnkit engine<float> fwd+bwd, {a.variant} H={a.hidden} NH={a.heads}, "
+                       f"B={a.batch} rows (one process each), T={a.cpu_sample_steps} steps, wall {wall:.2f} s"),
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if not O.Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref.so missing"}), flush=True)
+        return
+    pool, cores = make_pool(a)
+    T_s = a.cpu_sample_steps
+    try:
+        for _ in range(a.warmup):
+            cpu_reference_step(a, max(2, T_s // 8), pool, cores)
+        walls = []
+        for _ in range(a.steps):
+            _, w = cpu_reference_step(a, T_s, pool, cores)
+            walls.append(w)
+    finally:
+        pool.shutdown()
+    total = sum(walls)
+    value = a.batch * T_s * a.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (numpy RNG, reference distributions)",
+        "config": {"workload": workload_name(a), "batch_per_gpu": a.batch, "seq_len": a.seq,
+                   "hidden": a.hidden, "heads": a.heads, "sample_seq_len": T_s},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"B={a.batch} rows x T={T_s} steps per step, engine<float>",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- our impl ----
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2412_07752_b200 import FlashRNN
+    from paper_2412_07752_b200.abi import load, partition
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    eng = FlashRNN()
+    L = load()
+    L.frnn_debug_timing.argtypes = [C.c_int32]
+    L.frnn_debug_kernel_ms.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    shard = partition(a.seq, a.batch * world, a.heads, a.hidden // a.heads, world, rank)
+    inp = make_inputs(torch, dev, a, seed=rank)
+    ns, ng = NS_NG[a.variant]
+    D = a.hidden
+    st = torch.empty(a.seq + 1, ns, a.batch, D, dtype=torch.bfloat16, device=dev)
+    ga = torch.empty(a.seq, ng, a.batch, D, dtype=torch.bfloat16, device=dev)
+    out = dict(dx=torch.empty_like(inp["x"]), dbias=torch.empty_like(inp["bias"]),
+               dR=torch.empty_like(inp["R"]), ds0=torch.empty_like(inp["dsf"]))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.forward(a.variant, inp["R"], inp["bias"], inp["x"], inp["s0"], st, ga)
+        eng.backward(a.variant, inp["R"], inp["bias"], st, ga, inp["dsf"], out=out)
+        if world > 1:  # data-parallel parameter-gradient reduction (the only collective)
+            dist.all_reduce(out["dR"])
+            dist.all_reduce(out["dbias"])
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    L.frnn_debug_timing(1)
+    L.frnn_debug_kernel_ms(None, None)  # clear
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(a.steps):
+        flush.fill_(i & 0xFF)  # evict L2 between timed steps (outside the events)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms3 = (C.c_double * 3)()
+    cnt3 = (C.c_int64 * 3)()
+    L.frnn_debug_kernel_ms(ms3, cnt3)
+    L.frnn_debug_timing(0)
+    clk = clocks.stop()
+    total_ms = sum(s.elapsed_time(e) for s, e in ev)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = t.item()
+    ms_step = total_ms / a.steps
+    units = a.batch * a.seq * world
+    value = units / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (live CUDA-event timing) ----
+    names = ["forward recurrence (fused_fwd_kernel)", "backward recurrence (fused_bwd_kernel)",
+             "dR/db reduction (dr_db_kernel)"]
+    shares = [ms3[i] for i in range(3)]
+    dom = max(range(3), key=lambda i: shares[i])
+    peaks, peak_src = measured_peaks()
+    avg_ms = ms3[dom] / max(1, cnt3[dom])
+    fl = flops_per_pass(a)
+    achieved = fl / (avg_ms / 1e3) / 1e12
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(["fwd", "bwd", "param"][dom])
+    except Exception:
+        pass
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": names[dom], "avg_launch_ms": avg_ms,
+            "flops_per_launch": fl, "peak_source": f"{peak_src} bf16_tflops_sustained",
+            "step_share": shares[dom] / max(1e-9, total_ms),
+            "per_step_latency_us": {"forward": 1e3 * ms3[0] / max(1, cnt3[0]) / a.seq,
+                                    "backward": 1e3 * ms3[1] / max(1, cnt3[1]) / a.seq},
+            "kernel_ms_per_step": {"forward": ms3[0] / a.steps, "backward": ms3[1] / a.steps,
+                                   "param_grads": ms3[2] / a.steps}}
+
+    # ---- end to end through the C ABI with host buffers ----
+    host = {k: v.cpu().pin_memory() for k, v in inp.items()}
+    hout = {k: torch.empty(out[k].shape, dtype=out[k].dtype).pin_memory() for k in ("dR", "dbias", "ds0")}
+    dbuf = {k: torch.empty_like(v) for k, v in inp.items()}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = sum(v.numel() * v.element_size() for v in hout.values())
+
+    def e2e_step():
+        for k in host:
+            dbuf[k].copy_(host[k], non_blocking=True)
+        eng.forward(a.variant, dbuf["R"], dbuf["bias"], dbuf["x"], dbuf["s0"], st, ga)
+        eng.backward(a.variant, dbuf["R"], dbuf["bias"], st, ga, dbuf["dsf"], out=out)
+        if world > 1:
+            dist.all_reduce(out["dR"])
+            dist.all_reduce(out["dbias"])
+        for k in hout:
+            hout[k].copy_(out[k], non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    e2e = {"value": units * a.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        return
+    plan = {p: eng.plan(a.variant, a.seq, a.batch, a.heads, a.hidden // a.heads, "bf16", p)
+            for p in ("forward", "backward")}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (torch RNG on device, reference generator distributions)",
+        "config": {"workload": workload_name(a), "variant": a.variant, "batch_per_gpu": a.batch,
+                   "global_batch": a.batch * world, "seq_len": a.seq, "hidden": a.hidden, "heads": a.heads,
+                   "parallelism": f"batch-shard x{world} (frnn_partition: {shard})" if world > 1 else "single GPU",
+                   "l2": "flushed between timed steps (256 MB write, outside the events)"},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": int(sum(cnt3[i] for i in range(3))),
+        "clocks": clk,
+        "plan": {k: {kk: v[kk] for kk in ("algo", "grid", "ctas_per_group", "units_per_cta", "tmem_cols",
+                                          "smem_bytes", "solve_us") if kk in v}
+                 for k, v in plan.items()},
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,24 @@
+/*
+ * flashrnn_debug.h -- developer instrumentation for libflashrnn.so (not part of
+ * the drop-in boundary).
+ *
+ * frnn_debug_profile: when a device buffer is registered, the persistent
+ *   kernels record clock64() phase stamps for the first `steps` steps of every
+ *   CTA: buf[(cta * steps + step) * 8 + phase].  Pass NULL to disable.
+ * frnn_debug_timing / frnn_debug_kernel_ms: CUDA-event timing of each kernel
+ *   class on its launch stream -- [0] forward recurrence, [1] backward
+ *   recurrence, [2] dR/db reduction -- summed in ms with launch counts.
+ */
+#ifndef FLASHRNN_DEBUG_H_
+#define FLASHRNN_DEBUG_H_
+#include "flashrnn.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+FRNN_API int frnn_debug_profile(void* device_buffer, int32_t steps);
+FRNN_API int frnn_debug_timing(int32_t enable);
+FRNN_API int frnn_debug_kernel_ms(double* ms3, int64_t* count3);
+#ifdef __cplusplus
+}
+#endif
+#endif

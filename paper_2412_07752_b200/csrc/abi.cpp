@@ -13,8 +13,14 @@
 #include <tuple>
 
 #include "../../include/flashrnn.h"
+#include "../../include/flashrnn_debug.h"
 #include "kernels.h"
 #include "planner.h"
+
+namespace frnn {
+extern long long* g_prof_buf;
+extern int g_prof_steps;
+}  // namespace frnn
 
 namespace {
 
@@ -297,6 +303,12 @@ int frnn_partition(frnn_shape shape, int32_t world_size, int32_t rank, frnn_shar
   out->batch_begin = (int)((long long)shape.batch * bp / bs);
   out->batch_end = (int)((long long)shape.batch * (bp + 1) / bs);
   out->reduce_params = bs > 1;
+  return FRNN_OK;
+}
+
+int frnn_debug_profile(void* device_buffer, int32_t steps) {
+  frnn::g_prof_buf = static_cast<long long*>(device_buffer);
+  frnn::g_prof_steps = device_buffer ? steps : 0;
   return FRNN_OK;
 }
 

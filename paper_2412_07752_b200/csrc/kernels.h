@@ -49,6 +49,7 @@ cudaError_t simt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream
 cudaError_t fused_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 cudaError_t fused_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 size_t fused_forward_ws(const Problem& p, const Plan& pl);
+uint32_t fused_tmem_cols(const Problem& p, int N, bool backward);
 size_t fused_backward_ws(const Problem& p, const Plan& pl);
 
 // ---- alternating path (alternating.cu) ----
@@ -71,5 +72,10 @@ size_t param_grads_ws(const Problem& p);
 cudaError_t check_finite(const void* ptr, size_t n, bool bf16, int* flag, cudaStream_t s);
 
 int sm_count();
+
+// ---- optional per-kernel-class event timing (ktimer.cpp) ----
+enum KernelClass { KT_FWD = 0, KT_BWD = 1, KT_PARAM = 2, KT_N = 3 };
+void kt_begin(int cls, cudaStream_t s);
+void kt_end(int cls, cudaStream_t s);
 
 }  // namespace frnn

@@ -37,24 +37,16 @@ static int ngp_of(int NG) { return NG <= 1 ? 1 : NG <= 2 ? 2 : 4; }
 static bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
   const int NGP = ngp_of(p.NG);
   const int N = 16;
-  if (p.DH % 16) {
-    *why = "fused: head_dim must be a multiple of 16";
+  if (p.DH % 8) {
+    *why = "fused: head_dim must be a multiple of 8 (16-byte h chunks)";
     return false;
   }
   const int K = (int)align_up(p.DH, 32);
-  const int MB = (p.DH + 127) / 128;
   const int NBT = (p.B + N - 1) / N;
-  if (pass == 0) {
-    const int cols = (int)align_up(K / 2, 32) + N;
-    if (cols > lim.tmem_cols) {
-      *why = "fused forward: R slice + accumulator exceed TMEM";
-      return false;
-    }
-  } else {
-    if (MB * 64 + MB * N > lim.tmem_cols) {
-      *why = "fused backward: R^T slice + accumulators exceed TMEM";
-      return false;
-    }
+  if ((int)fused_tmem_cols(p, N, pass == 1) > lim.tmem_cols) {
+    *why = pass == 0 ? "fused forward: R slice + accumulators exceed TMEM"
+                     : "fused backward: R^T slice + accumulators exceed TMEM";
+    return false;
   }
   const size_t smem = pass == 0 ? (size_t)N * K * 2 + 128 * (N + 1) * 4 + 16 : (size_t)N * 128 * 2 + 16;
   if ((int)smem > lim.smem_optin) {
@@ -85,10 +77,7 @@ static bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan
   pl.grid = grid;
   pl.threads = 128;
   pl.smem_bytes = (int)smem;
-  int need = pass == 0 ? (int)align_up(K / 2, 32) + N : MB * 64 + MB * N;
-  int cols = 32;
-  while (cols < need) cols <<= 1;
-  pl.tmem_cols = cols;
+  pl.tmem_cols = (int)fused_tmem_cols(p, N, pass == 1);
   pl.k_split = 1;
   pl.ws_bytes = pass == 0 ? fused_forward_ws(p, pl) : fused_backward_ws(p, pl);
   return true;

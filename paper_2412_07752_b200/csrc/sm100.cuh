@@ -93,6 +93,15 @@ __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// One lane of a converged warp (elect.sync).  Issuing tcgen05 from a full warp
+// under this predicate, with warp-uniform operands, lets ptxas keep operands in
+// uniform registers -- no per-instruction ELECT/BRA.U.ANY "waterfall" loop.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05.mma complete.
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
   asm volatile(
