@@ -48,6 +48,7 @@ struct FArgs {
   uint32_t* flags;  // [groups][CPG] step counters (one writer each)
   float* part;      // backward partials [2][groups][CPG][MB*128][N]
   bf16* dgw;        // backward dg trace (only when a gate is not input-wired)
+  float* dbacc;     // backward db accumulator [NG][D] fp32 (tcgen05 dR path)
   long long* prof;  // optional per-step phase timestamps (clock64), thread 0 of each CTA
   int prof_steps;
 };
@@ -362,8 +363,10 @@ __global__ void __launch_bounds__(128, 1) fused_bwd_kernel(FArgs a) {
   const int u = w * UPW + uw;
   const bool own = u < a.UPC;
   const int e = hd * DH + unit0 + (own ? u : 0);
-  float ds[NS][EPT];
+  float ds[NS][EPT], dbv[NG];  // dbv: this thread's share of db (engine.hpp:317)
   unsigned short pv[NS][EPT], gv[NG][EPT], hv[EPT];
+#pragma unroll
+  for (int j = 0; j < NG; ++j) dbv[j] = 0.f;
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int b = bo * EPT + i;
@@ -451,6 +454,7 @@ __global__ void __launch_bounds__(128, 1) fused_bwd_kernel(FArgs a) {
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
           dgv[j][i] = dg[j];
+          if (b < nb) dbv[j] += dg[j];
           if (b < nb)
             *reinterpret_cast<bf16*>(dgB + kmaj_off<N>(b, 32 * w + uw * NGP + j)) = __float2bfloat16_rn(dg[j]);
         }
@@ -537,6 +541,15 @@ __global__ void __launch_bounds__(128, 1) fused_bwd_kernel(FArgs a) {
       for (int s = 0; s < NS; ++s) ds0[((size_t)s * B + b0 + b) * D + e] = __float2bfloat16_rn(ds[s][i]);
     }
   }
+  if (a.dbacc) {  // db: sum this unit's batch shares across lanes, one fp32 atomic per (gate, unit, tile)
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      float v = dbv[j];
+#pragma unroll
+      for (int off = UPW; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (own && bo == 0) atomicAdd(a.dbacc + (size_t)j * D + e, v);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc(tbase, a.tmem_cols);
@@ -602,7 +615,11 @@ FArgs make_args(const Problem& p, const Plan& pl, void* ws, bool backward) {
     off += align_up(sizeof(float) * 2 * a.groups * a.CPG * (size_t)a.MB * 128 * N, 256);
     bool all_in = true;
     for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
-    a.dgw = all_in ? nullptr : reinterpret_cast<bf16*>(w + off);
+    if (!all_in) {
+      a.dgw = reinterpret_cast<bf16*>(w + off);
+      off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
+    }
+    a.dbacc = dr_gemm_supported(p) ? reinterpret_cast<float*>(w + off) : nullptr;
   }
   return a;
 }
@@ -638,6 +655,7 @@ size_t fused_backward_ws(const Problem& p, const Plan& pl) {
   bool all_in = true;
   for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
   if (!all_in) off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
+  off += align_up(sizeof(float) * p.NG * p.D, 256);  // db accumulator
   return off;
 }
 
@@ -667,15 +685,21 @@ cudaError_t fused_backward(const Problem& p, const Plan& pl, void* ws, cudaStrea
   if (e != cudaSuccess) return e;
   const size_t smem = bwd_smem(pl.batch_tile);
   if (pl.batch_tile != 16) return cudaErrorInvalidValue;
+  if (a.dbacc && (e = cudaMemsetAsync(a.dbacc, 0, sizeof(float) * p.NG * p.D, s)) != cudaSuccess) return e;
   kt_begin(KT_BWD, s);
   FRNN_FUSED_DISPATCH(fused_bwd_kernel, 16)
   kt_end(KT_BWD, s);
   if (e != cudaSuccess) return e;
   // dR / db from the dg trace (dx when every gate is input-wired).
-  DgView dg{a.dgw ? static_cast<const void*>(a.dgw) : p.dx, (long long)p.B * p.NG * p.D,
-            (long long)p.NG * p.D, (long long)p.D};
+  const void* dgp = a.dgw ? static_cast<const void*>(a.dgw) : p.dx;
   kt_begin(KT_PARAM, s);
-  e = param_grads(p, dg, nullptr, s);
+  if (a.dbacc) {  // tcgen05 GEMM for dR; db was accumulated by the recurrence
+    e = dr_gemm(p, dgp, s);
+    if (e == cudaSuccess) e = db_convert(a.dbacc, p.dbias, p.NG * p.D, s);
+  } else {
+    DgView dg{dgp, (long long)p.B * p.NG * p.D, (long long)p.NG * p.D, (long long)p.D};
+    e = param_grads(p, dg, nullptr, s);
+  }
   kt_end(KT_PARAM, s);
   return e;
 }

@@ -67,6 +67,11 @@ struct DgView {
 cudaError_t param_grads(const Problem& p, DgView dg, void* ws, cudaStream_t s);
 size_t param_grads_ws(const Problem& p);
 
+// ---- tcgen05 dR GEMM (dr_gemm.cu) ----
+bool dr_gemm_supported(const Problem& p);
+cudaError_t dr_gemm(const Problem& p, const void* dg_dx_layout, cudaStream_t s);
+cudaError_t db_convert(const float* acc, void* db, int n, cudaStream_t s);
+
 // ---- utilities (util.cu) ----
 // Sets *flag (device int) to 1 if any of the n elements is non-finite.
 cudaError_t check_finite(const void* ptr, size_t n, bool bf16, int* flag, cudaStream_t s);
