@@ -119,6 +119,7 @@ typedef struct {
   int32_t k_split;           /* accumulating-axis split (alternating path) */
   int64_t workspace_bytes;   /* scratch the pass needs */
   double solve_us;           /* solver wall time */
+  int32_t cluster;           /* >0: thread-block cluster size of the cluster-resident fused kernels */
 } frnn_plan_info;
 
 /* -- metadata ----------------------------------------------------------- */

@@ -52,7 +52,8 @@ class PlanInfo(C.Structure):
     _fields_ = [("algo", C.c_int32), ("rows_per_cta", C.c_int32), ("batch_tile", C.c_int32),
                 ("ctas_per_group", C.c_int32), ("groups", C.c_int32), ("grid", C.c_int32),
                 ("threads", C.c_int32), ("smem_bytes", C.c_int32), ("tmem_cols", C.c_int32),
-                ("k_split", C.c_int32), ("workspace_bytes", C.c_int64), ("solve_us", C.c_double)]
+                ("k_split", C.c_int32), ("workspace_bytes", C.c_int64), ("solve_us", C.c_double),
+                ("cluster", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -176,6 +176,7 @@ int frnn_plan(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pa
   out->smem_bytes = pl.smem_bytes;
   out->tmem_cols = pl.tmem_cols;
   out->k_split = pl.k_split;
+  out->cluster = pl.cluster;
   out->workspace_bytes = (int64_t)pl.ws_bytes;
   out->solve_us = pl.solve_us;
   return FRNN_OK;
@@ -233,7 +234,9 @@ int frnn_forward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const v
   }
   switch (pl.algo) {
     case FRNN_ALGO_SIMT: e = frnn::simt_forward(p, pl, workspace, s); break;
-    case FRNN_ALGO_FUSED: e = frnn::fused_forward(p, pl, workspace, s); break;
+    case FRNN_ALGO_FUSED:
+      e = pl.cluster ? frnn::cluster_forward(p, pl, workspace, s) : frnn::fused_forward(p, pl, workspace, s);
+      break;
     default: e = frnn::alt_forward(p, pl, workspace, s); break;
   }
   if (e == cudaErrorNotSupported) return fail(FRNN_EUNSUPPORTED, "algorithm not implemented for this shape");
@@ -276,7 +279,9 @@ int frnn_backward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const 
     return fail(FRNN_EINVAL_ARG, "workspace too small: need " + std::to_string(need) + " bytes");
   switch (pl.algo) {
     case FRNN_ALGO_SIMT: e = frnn::simt_backward(p, pl, workspace, s); break;
-    case FRNN_ALGO_FUSED: e = frnn::fused_backward(p, pl, workspace, s); break;
+    case FRNN_ALGO_FUSED:
+      e = pl.cluster ? frnn::cluster_backward(p, pl, workspace, s) : frnn::fused_backward(p, pl, workspace, s);
+      break;
     default: e = frnn::alt_backward(p, pl, workspace, s); break;
   }
   if (e == cudaErrorNotSupported) return fail(FRNN_EUNSUPPORTED, "algorithm not implemented for this shape");

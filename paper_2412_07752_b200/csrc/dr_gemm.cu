@@ -142,9 +142,13 @@ __global__ void __launch_bounds__(128, 1) dr_gemm_kernel(const __grid_constant__
   if (w == 0) tmem_dealloc(tbase, BN <= 64 ? 64 : BN <= 128 ? 128 : 256);
 }
 
-__global__ void db_convert_kernel(const float* acc, bf16* db, int n) {
+__global__ void db_convert_kernel(const float* acc, bf16* db, int n, int tiles) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) db[i] = __float2bfloat16_rn(acc[i]);
+  if (i < n) {
+    float s = 0.f;
+    for (int t = 0; t < tiles; ++t) s += acc[(size_t)t * n + i];
+    db[i] = __float2bfloat16_rn(s);
+  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -222,8 +226,8 @@ cudaError_t dr_gemm(const Problem& p, const void* dg, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t db_convert(const float* acc, void* db, int n, cudaStream_t s) {
-  db_convert_kernel<<<(n + 255) / 256, 256, 0, s>>>(acc, static_cast<bf16*>(db), n);
+cudaError_t db_convert(const float* acc, void* db, int n, int tiles, cudaStream_t s) {
+  db_convert_kernel<<<(n + 255) / 256, 256, 0, s>>>(acc, static_cast<bf16*>(db), n, tiles);
   return cudaGetLastError();
 }
 

@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(128, 1) fused_bwd_kernel(FArgs a) {
       float v = dbv[j];
 #pragma unroll
       for (int off = UPW; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (own && bo == 0) atomicAdd(a.dbacc + (size_t)j * D + e, v);
+      if (own && bo == 0) a.dbacc[((size_t)(grp % a.NBT) * NG + j) * D + e] = v;  // one writer per (tile, gate, unit)
     }
   }
   tc_fence_before();
@@ -655,7 +655,7 @@ size_t fused_backward_ws(const Problem& p, const Plan& pl) {
   bool all_in = true;
   for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
   if (!all_in) off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
-  off += align_up(sizeof(float) * p.NG * p.D, 256);  // db accumulator
+  off += align_up(sizeof(float) * ((p.B + N - 1) / N) * p.NG * p.D, 256);  // db per batch tile
   return off;
 }
 
@@ -685,7 +685,6 @@ cudaError_t fused_backward(const Problem& p, const Plan& pl, void* ws, cudaStrea
   if (e != cudaSuccess) return e;
   const size_t smem = bwd_smem(pl.batch_tile);
   if (pl.batch_tile != 16) return cudaErrorInvalidValue;
-  if (a.dbacc && (e = cudaMemsetAsync(a.dbacc, 0, sizeof(float) * p.NG * p.D, s)) != cudaSuccess) return e;
   kt_begin(KT_BWD, s);
   FRNN_FUSED_DISPATCH(fused_bwd_kernel, 16)
   kt_end(KT_BWD, s);
@@ -695,7 +694,7 @@ cudaError_t fused_backward(const Problem& p, const Plan& pl, void* ws, cudaStrea
   kt_begin(KT_PARAM, s);
   if (a.dbacc) {  // tcgen05 GEMM for dR; db was accumulated by the recurrence
     e = dr_gemm(p, dgp, s);
-    if (e == cudaSuccess) e = db_convert(a.dbacc, p.dbias, p.NG * p.D, s);
+    if (e == cudaSuccess) e = db_convert(a.dbacc, p.dbias, p.NG * p.D, a.NBT, s);
   } else {
     DgView dg{dgp, (long long)p.B * p.NG * p.D, (long long)p.NG * p.D, (long long)p.D};
     e = param_grads(p, dg, nullptr, s);

@@ -1,0 +1,734 @@
+// fused_cluster.cu -- cluster-resident persistent recurrence kernels (bf16):
+// K1c forward (engine.hpp:170-201) and K2c backward (engine.hpp:257-336).
+//
+// One thread-block cluster per group (head x batch tile of N=16 rows); CL CTAs
+// per cluster, each owning UPC hidden units and all NG gates of them
+// (row = u*NGP + g), so the cell update is CTA-local.  R stays on-chip for
+// all T steps: rows [0,R1) in TMEM (A operand of tcgen05.mma kind::f16 'TS'),
+// rows [R1,R1+R2) (R2 <= 64) in SMEM (an M=64 'SS' MMA).  For H=768, NG=4:
+// CL=16, UPC=48, R1=128, R2=64 -- 4.7 MB of R spread over 16 SMs.
+//
+// Per forward step the only inter-CTA traffic is h: each CTA writes its
+// [UPC x N] bf16 slice (already in the MMA's K-major core-matrix layout) to a
+// global staging buffer and ONE thread issues a TMA multicast that drops it
+// into every CTA's double-buffered B tile, completing bytes on each CTA's
+// mbarrier.  No flag polling through L2: a CTA's MMA for step t+1 starts when
+// its mbarrier has counted all CL slices.  (All-gather of 24 KB in a 16-CTA
+// cluster: ~890 cycles measured, vs ~5-6k for release/acquire flags + loads;
+// profiles/r01_allgather_microbench.txt.)
+//
+// Per backward step each CTA computes the partial R_p^T dg_p for all DH state
+// columns (A = R_p^T resident: MBT 128-column blocks in TMEM, the rest in SMEM),
+// stores it fp32 to global staging laid out [dest][src][b][u], and releases one
+// remote mbarrier arrive to every CTA; each CTA then pulls its [all src] block
+// with one TMA bulk load and sums the CL partials (+ clip, engine.hpp:300-303).
+//
+// Element work: NT = up to 384 threads (3 warps per scheduler, so ALU/MUFU
+// latencies overlap); each thread owns a PAIR of adjacent units of one batch
+// row, so trace/x/dx traffic is bf16x2 and the dg tile gets 16-byte stores.
+// MMAs are issued by warp 0 as whole-warp PTX loops (sm100.cuh mma_chain_*).
+#include <cuda_bf16.h>
+
+#include "cells.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace frnn {
+
+extern long long* g_prof_buf;
+extern int g_prof_steps;
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+using namespace sm100;
+
+constexpr int MAXT = 384;
+
+struct CArgs {
+  Problem p;
+  int UPC, CL, NBT;
+  int R1, R2;      // forward: rows in the TMEM block / the SMEM (M=64) block
+  int K;           // forward contraction = DH (multiple of 16)
+  int KBP;         // backward contraction = UPC*NGP padded to 16
+  int MB, MBT;     // backward: 128-column blocks of DH / how many have A in TMEM
+  uint32_t tmem_cols, acc1, acc2;
+  uint32_t slice;  // forward: bytes of one CTA's h slice
+  bf16* xstage;    // forward staging [groups][2][CL][slice]
+  float* pstage;   // backward staging [groups][2][CL dest][CL src][N][UPC]
+  bf16* dgw;
+  float* dbacc;    // [NBT][NG][D]
+  long long* prof;
+  int prof_steps;
+};
+
+#define FRNN_PROF(slot, step)                                              \
+  if (a.prof && threadIdx.x == 0 && (step) < a.prof_steps)                 \
+    a.prof[((size_t)blockIdx.x * a.prof_steps + (step)) * 8 + (slot)] = clock64();
+
+__device__ __forceinline__ float bf(const bf16* p, size_t i) { return __bfloat162float(p[i]); }
+__device__ __forceinline__ float lo16(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float hi16(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t ld2(const bf16* p, size_t i) { return *reinterpret_cast<const uint32_t*>(p + i); }
+__device__ __forceinline__ void st2(bf16* p, size_t i, float lo, float hi) {
+  *reinterpret_cast<uint32_t*>(p + i) = pack_bf16(lo, hi);
+}
+
+// K-major, no-swizzle operand tile with `rows` rows: core matrix (k/8, r/8).
+__device__ __forceinline__ uint32_t kmaj(int r, int k, int rows) {
+  return (uint32_t)(((k >> 3) * (rows >> 3) + (r >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
+// ------------------------------------------------------------ forward ----
+template <int V, int N>
+__global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
+  using C = Cell<V>;
+  constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP;
+  using M = Math<true>;
+  const Problem& p = a.p;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, NT = blockDim.x;
+  const uint32_t me = cluster_ctarank();
+  const int grp = blockIdx.x / a.CL;
+  const int hd = grp / a.NBT, b0 = (grp % a.NBT) * N;
+  const int nb = min(N, p.B - b0);
+  const int unit0 = me * a.UPC;
+  const int DH = p.DH, D = p.D, B = p.B, K = a.K, T = p.T;
+  const int ROWS = a.R1 + a.R2, XP = ROWS + 1;
+  const bf16* R = static_cast<const bf16*>(p.R);
+  const bf16* bias = static_cast<const bf16*>(p.bias);
+  const bf16* x = static_cast<const bf16*>(p.x);
+  const bf16* s0 = static_cast<const bf16*>(p.s0);
+  bf16* states = static_cast<bf16*>(p.states);
+  bf16* gates = static_cast<bf16*>(p.gates);
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* hB0 = smem;                       // [N x K] K-major (step parity 0)
+  uint8_t* hB1 = hB0 + N * K * 2;            // (step parity 1)
+  uint8_t* A2 = hB1 + N * K * 2;             // [64 x K] K-major, rows R1..R1+R2
+  float* xs = reinterpret_cast<float*>(A2 + (a.R2 ? 64 * K * 2 : 0));  // [N][ROWS+1]
+  uint8_t* hs = reinterpret_cast<uint8_t*>(xs + N * XP);               // my h slice
+  uint64_t* bars = reinterpret_cast<uint64_t*>(hs + ((a.slice + 15) & ~15u));  // mma, x0, x1
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bars + 3);
+
+  if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < 2 * N * K * 2 / 16; i += NT) reinterpret_cast<uint4*>(hB0)[i] = make_uint4(0, 0, 0, 0);
+  if (a.R2) {  // R rows R1.. -> SMEM, K-major M=64 tile
+    for (int i = tid; i < 64 * (K / 8); i += NT) {
+      const int m = i % 64, kc = i / 64, r = a.R1 + m, u = r / NGP, g = r % NGP;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (m < a.R2 && g < NG && p.rec[g])
+        v = *reinterpret_cast<const uint4*>(R + ((size_t)(hd * NG + g) * DH + unit0 + u) * DH + kc * 8);
+      *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, 64)) = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tbase_s, 0);
+  if (w < 4) {  // R rows 0..R1-1 -> TMEM: lane = row, columns = bf16 pairs along K
+    const int row = 32 * w + l, u = row / NGP, g = row % NGP;
+    const bool valid = row < a.R1 && g < NG && p.rec[g];
+    const bf16* src = R + ((size_t)(hd * NG + (valid ? g : 0)) * DH + unit0 + (valid ? u : 0)) * DH;
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 2 * c0 + 8 * q;
+        uint4 r4 = make_uint4(0, 0, 0, 0);
+        if (valid && k < DH) r4 = *reinterpret_cast<const uint4*>(src + k);
+        v[4 * q] = r4.x;
+        v[4 * q + 1] = r4.y;
+        v[4 * q + 2] = r4.z;
+        v[4 * q + 3] = r4.w;
+      }
+      tmem_st16(tbase + ((uint32_t)(32 * w) << 16) + c0, v);
+    }
+    tmem_st_wait();
+  }
+  // ---- element ownership: one pair (u, u+1) of one batch row b per thread
+  const int NP = a.UPC / 2;
+  const bool own = tid < NP * N;
+  const int u = 2 * (tid % NP), b = tid / NP;
+  const bool valid = own && b < nb;
+  const int e = hd * DH + unit0 + u;
+  const size_t so = (size_t)(b0 + b) * D + e;       // offset in [.][B][D] tensors
+  const size_t xo = (size_t)(b0 + b) * NG * D + e;  // offset in [.][B][NG][D] tensors
+  const size_t sstep = (size_t)NS * B * D, gstep = (size_t)NG * B * D;
+  float st[NS][2], bj[NG][2];
+  uint32_t xr[NG];
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    bj[j][0] = own ? bf(bias, (size_t)j * D + e) : 0.f;
+    bj[j][1] = own ? bf(bias, (size_t)j * D + e + 1) : 0.f;
+    xr[j] = 0;
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const uint32_t v = valid ? ld2(s0, (size_t)s * B * D + so) : 0u;
+    st[s][0] = lo16(v);
+    st[s][1] = hi16(v);
+    if (valid) *reinterpret_cast<uint32_t*>(states + (size_t)s * B * D + so) = v;  // states[0] = s0
+  }
+  if (valid && T > 0) {
+#pragma unroll
+    for (int j = 0; j < NG; ++j)
+      if (p.inp[j]) xr[j] = ld2(x, xo + (size_t)j * D);
+  }
+  // h_0 tile straight from s0 into hB0
+  for (int i = tid; i < nb * (K / 8); i += NT) {
+    const int bb = i % nb, kc = i / nb;
+    *reinterpret_cast<uint4*>(hB0 + kmaj(bb, kc * 8, N)) =
+        *reinterpret_cast<const uint4*>(s0 + (size_t)(b0 + bb) * D + hd * DH + kc * 8);
+  }
+  fence_proxy_async_smem();
+  if (tid == 0) mbar_arrive_expect_tx(&bars[2], (uint32_t)a.CL * a.slice);  // step 1's h
+  __syncthreads();
+  cluster_sync_all();  // all barriers initialised + armed before any multicast
+
+  const uint32_t idesc1 = idesc_bf16(128, N), idesc2 = idesc_bf16(64, N);
+  constexpr uint32_t LBO = N * 16, SBO = 128;
+  const uint16_t mask = (uint16_t)((1u << a.CL) - 1u);
+  for (int t = 0; t < T; ++t) {
+    const int buf = t & 1;
+    FRNN_PROF(0, t);
+    if (w == 0) {
+      if (t > 0) mbar_wait_cluster(&bars[1 + buf], ((t - 1) >> 1) & 1);
+      FRNN_PROF(1, t);
+      tc_fence_after();
+      const uint64_t bd = sdesc_kmajor(smem_u32(buf ? hB1 : hB0), LBO, SBO);
+      if (a.R2)
+        mma_chain_ts_ss(tbase + a.acc1, tbase, 8, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
+                        (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, K / 16);
+      else
+        mma_chain_ts(tbase + a.acc1, tbase, 8, bd, (2 * LBO) >> 4, idesc1, K / 16);
+      if (elect_one()) mma_commit(&bars[0]);
+      __syncwarp();
+    }
+    mbar_wait(&bars[0], t & 1);
+    tc_fence_after();
+    FRNN_PROF(2, t);
+    if (w < 4) {  // accumulators -> xs[b][row]
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc1, v);
+      if (32 * w + l < a.R1) {
+#pragma unroll
+        for (int n = 0; n < N; ++n) xs[n * XP + 32 * w + l] = v[n];
+      }
+      if (a.R2) {  // M=64 layout: rows 16w..16w+15 in lanes 32w..32w+15
+        tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc2, v);
+        if (l < 16 && 16 * w + l < a.R2) {
+#pragma unroll
+          for (int n = 0; n < N; ++n) xs[n * XP + a.R1 + 16 * w + l] = v[n];
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    float gout[NG][2], nout[NS][2];
+    if (own) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float g[4], prev[4], nx[4];
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {  // x, then b, then y (engine.hpp:183-187)
+          g[j] = (h ? hi16(xr[j]) : lo16(xr[j])) + bj[j][h] + xs[b * XP + (u + h) * NGP + j];
+          gout[j][h] = g[j];
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) prev[s] = st[s][h];
+        C::template fwd<M>(prev, g, nx);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) st[s][h] = nout[s][h] = nx[s];
+      }
+      *reinterpret_cast<uint32_t*>(hs + kmaj(b, u, N)) =
+          b < nb ? pack_bf16(nout[0][0], nout[0][1]) : 0u;  // padding rows stay zero
+    }
+    __syncthreads();
+    FRNN_PROF(3, t);
+    if (t + 1 < T) {  // publish h_{t+1}: slice -> global staging -> multicast to the cluster
+      const int nbuf = (t + 1) & 1;
+      uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + nbuf) * a.CL + me) * a.slice;
+      for (int i = tid; i < (int)(a.slice / 16); i += NT)
+        reinterpret_cast<uint4*>(gst)[i] = reinterpret_cast<const uint4*>(hs)[i];
+      fence_proxy_async_global();
+      __syncthreads();
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&bars[1 + buf], (uint32_t)a.CL * a.slice);  // re-arm for step t+2
+        fence_proxy_async_global();
+        bulk_g2s_multicast((nbuf ? hB1 : hB0) + me * a.slice, gst, a.slice, &bars[1 + nbuf], mask);
+      }
+    }
+    FRNN_PROF(4, t);
+    // Off the critical path: the trace, and x_{t+1} (bf16x2 accesses).
+    if (valid) {
+      bf16* gdst = gates + (size_t)t * gstep + so;
+      bf16* sdst = states + (size_t)(t + 1) * sstep + so;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) st2(gdst, (size_t)j * B * D, gout[j][0], gout[j][1]);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) st2(sdst, (size_t)s * B * D, nout[s][0], nout[s][1]);
+      if (t + 1 < T) {
+        const bf16* xn = x + (size_t)(t + 1) * gstep + xo;
+#pragma unroll
+        for (int j = 0; j < NG; ++j)
+          if (p.inp[j]) xr[j] = ld2(xn, (size_t)j * D);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer's multicast may target it
+  if (w == 0) tmem_dealloc(tbase, a.tmem_cols);
+}
+
+// ----------------------------------------------------------- backward ----
+template <int V, int N>
+__global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
+  using C = Cell<V>;
+  constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP;
+  using M = Math<true>;
+  const Problem& p = a.p;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, NT = blockDim.x;
+  const uint32_t me = cluster_ctarank();
+  const int grp = blockIdx.x / a.CL;
+  const int hd = grp / a.NBT, b0 = (grp % a.NBT) * N;
+  const int nb = min(N, p.B - b0);
+  const int unit0 = me * a.UPC;
+  const int DH = p.DH, D = p.D, B = p.B, T = p.T, KBP = a.KBP, MB = a.MB, MBT = a.MBT;
+  const bool recur = p.clip_mode != 2;
+  const float mag = p.clip_mag;
+  const bf16* R = static_cast<const bf16*>(p.R);
+  const bf16* states = static_cast<const bf16*>(p.cstates);
+  const bf16* gates = static_cast<const bf16*>(p.cgates);
+  const bf16* dsf = static_cast<const bf16*>(p.dsf);
+  const bf16* dh = static_cast<const bf16*>(p.dh);
+  bf16* dx = static_cast<bf16*>(p.dx);
+  bf16* ds0 = static_cast<bf16*>(p.ds0);
+  const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * 4;
+  const size_t blk_bytes = (size_t)128 * KBP * 2;
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* AS = smem;                                                    // (MB-MBT) x [128 x KBP] K-major
+  float* recv = reinterpret_cast<float*>(AS + (MB - MBT) * blk_bytes);  // [CL src][N][UPC]
+  uint8_t* dgB = reinterpret_cast<uint8_t*>(recv) + recv_bytes;         // [N x KBP] K-major
+  float* dbs = reinterpret_cast<float*>(dgB + N * KBP * 2);             // [NG][N][UPC] db scratch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dbs + NG * N * a.UPC);   // mma, rcv, rdy0, rdy1
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bars + 4);
+
+  if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], a.CL);
+    mbar_init(&bars[3], a.CL);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < N * KBP * 2 / 16; i += NT) reinterpret_cast<uint4*>(dgB)[i] = make_uint4(0, 0, 0, 0);
+  if (recur) {  // R_slice^T blocks in SMEM: element (column m, row k) of block mb
+    for (int mb = MBT; mb < MB; ++mb) {
+      uint8_t* blk = AS + (mb - MBT) * blk_bytes;
+      for (int i = tid; i < 128 * KBP; i += NT) {
+        const int m = i % 128, k = i / 128, c = mb * 128 + m, uu = k / NGP, g = k % NGP;
+        const float v = (c < DH && uu < a.UPC && g < NG && p.rec[g])
+                            ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
+        *reinterpret_cast<bf16*>(blk + kmaj(m, k, 128)) = __float2bfloat16_rn(v);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tbase_s, 0);
+  if (recur && w < 4) {  // R_slice^T blocks in TMEM: lane = state column, columns = row pairs
+    for (int mb = 0; mb < MBT; ++mb) {
+      const int c = mb * 128 + 32 * w + l;
+      for (int c0 = 0; c0 < KBP / 2; c0 += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float f[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = 2 * (c0 + q) + h, uu = row / NGP, g = row % NGP;
+            f[h] = (c < DH && uu < a.UPC && g < NG && p.rec[g])
+                       ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
+          }
+          v[q] = pack_bf16(f[0], f[1]);
+        }
+        tmem_st16(tbase + ((uint32_t)(32 * w) << 16) + mb * (KBP / 2) + c0, v);
+      }
+    }
+    tmem_st_wait();
+  }
+  fence_proxy_async_smem();
+  // ---- element ownership: one pair (u, u+1) of one batch row b per thread
+  const int NP = a.UPC / 2;
+  const bool own = tid < NP * N;
+  const int u = 2 * (tid % NP), b = tid / NP;
+  const bool valid = own && b < nb;
+  const int e = hd * DH + unit0 + u;
+  const size_t so = (size_t)(b0 + b) * D + e;       // [.][B][D]
+  const size_t xo = (size_t)(b0 + b) * p.NG * D + e;  // [.][B][NG][D]
+  const size_t sstep = (size_t)NS * B * D, gstep = (size_t)NG * B * D;
+  float ds[NS][2], dbv[NG][2];
+  uint32_t pv[NS], gv[NG], hv = 0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const uint32_t v = valid ? ld2(dsf, (size_t)s * B * D + so) : 0u;
+    ds[s][0] = lo16(v);
+    ds[s][1] = hi16(v);
+    pv[s] = 0;
+  }
+#pragma unroll
+  for (int j = 0; j < NG; ++j) {
+    dbv[j][0] = dbv[j][1] = 0.f;
+    gv[j] = 0;
+  }
+  // Predicated loads (no select on the loaded value): issuing the prefetch
+  // never waits for it.
+  auto prefetch = [&](int t) {
+    if (valid && t >= 0) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) pv[s] = ld2(states, (size_t)t * sstep + (size_t)s * B * D + so);
+#pragma unroll
+      for (int j = 0; j < NG; ++j) gv[j] = ld2(gates, (size_t)t * gstep + (size_t)j * B * D + so);
+      if (dh) hv = ld2(dh, (size_t)t * B * D + so);
+    }
+  };
+  prefetch(T - 1);
+  __syncthreads();
+  cluster_sync_all();  // barrier inits visible before any remote arrive
+
+  // Partials of step s are in pstage[grp][s&1][me][*]: wait for the CL
+  // producers, pull them with one bulk load, sum, clip, add to ds_h.
+  uint32_t rcv_phase = 0;
+  auto absorb = [&](int s) {
+    const int pb = s & 1;
+    const int kpub = T - 1 - s;  // publish order of step s
+    if (w == 0) {
+      mbar_wait_cluster(&bars[2 + pb], (uint32_t)(kpub >> 1) & 1u);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&bars[1], recv_bytes);
+        bulk_g2s(recv, a.pstage + (((size_t)grp * 2 + pb) * a.CL + me) * a.CL * N * a.UPC, recv_bytes, &bars[1]);
+      }
+      __syncwarp();
+    }
+    mbar_wait(&bars[1], rcv_phase);
+    rcv_phase ^= 1;
+    if (own) {
+      float t0 = 0.f, t1 = 0.f;
+      const float* rp = recv + (size_t)b * a.UPC + u;
+      const size_t qs = (size_t)N * a.UPC;
+      for (int q = 0; q < a.CL; ++q) {
+        const float2 v = *reinterpret_cast<const float2*>(rp + q * qs);
+        t0 += v.x;
+        t1 += v.y;
+      }
+      if (p.clip_mode == 1) {
+        t0 = fminf(fmaxf(t0, -mag), mag);
+        t1 = fminf(fmaxf(t1, -mag), mag);
+      }
+      ds[0][0] += t0;
+      ds[0][1] += t1;
+    }
+    __syncthreads();  // recv is reloaded next step
+  };
+
+  const uint32_t idesc = idesc_bf16(128, N);
+  constexpr uint32_t LBO = N * 16, SBO = 128;
+  uint32_t mma_phase = 0;
+  for (int t = T - 1; t >= 0; --t) {
+    const int k = T - 1 - t;
+    FRNN_PROF(0, k);
+    if (recur && t + 1 < T) absorb(t + 1);
+    FRNN_PROF(1, k);
+    float dgv[NG][2];
+    if (own) {
+      uint32_t pk[2][2] = {{0u, 0u}, {0u, 0u}};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float prev[4], g[4], dsl[4], dg[4], dsp[4];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          prev[s] = h ? hi16(pv[s]) : lo16(pv[s]);
+          dsl[s] = ds[s][h];
+        }
+        dsl[0] += h ? hi16(hv) : lo16(hv);  // engine.hpp:258-263
+#pragma unroll
+        for (int j = 0; j < NG; ++j) g[j] = h ? hi16(gv[j]) : lo16(gv[j]);
+        C::template bwd<M>(prev, g, dsl, dg, dsp);
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+          const float d = b < nb ? dg[j] : 0.f;
+          dgv[j][h] = d;
+          dbv[j][h] += d;
+          pk[h][j >> 1] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d)) << (16 * (j & 1));
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) ds[s][h] = dsp[s];
+      }
+      // The pair's NGP*2 gate rows are contiguous along K of the dg tile.
+      if (NGP == 4)
+        *reinterpret_cast<uint4*>(dgB + kmaj(b, u * 4, N)) = make_uint4(pk[0][0], pk[0][1], pk[1][0], pk[1][1]);
+      else if (NGP == 2)
+        *reinterpret_cast<uint2*>(dgB + kmaj(b, u * 2, N)) = make_uint2(pk[0][0], pk[1][0]);
+      else
+        *reinterpret_cast<uint32_t*>(dgB + kmaj(b, u, N)) = (pk[0][0] & 0xFFFFu) | (pk[1][0] << 16);
+    }
+    prefetch(t - 1);
+    if (recur) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      FRNN_PROF(2, k);
+      if (w == 0) {  // TMEM-A blocks then SMEM-A blocks, whole-warp PTX chains
+        tc_fence_after();
+        const uint64_t bd = sdesc_kmajor(smem_u32(dgB), LBO, SBO);
+        const uint64_t ad = sdesc_kmajor(smem_u32(AS), 128 * 16, 128);
+        const int nk = KBP / 16, cb = KBP / 2;
+        for (int mb = 0; mb < MBT; ++mb)
+          mma_chain_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
+        for (int mb = MBT; mb < MB; ++mb)
+          mma_chain_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)), (2 * 128 * 16) >> 4,
+                       bd, (2 * LBO) >> 4, idesc, nk);
+        if (elect_one()) mma_commit(&bars[0]);
+        __syncwarp();
+      }
+      mbar_wait(&bars[0], mma_phase);
+      mma_phase ^= 1;
+      tc_fence_after();
+      FRNN_PROF(3, k);
+      // partial R_p^T dg_p, column c -> owner CTA c / UPC, layout [dest][src][b][u];
+      // every warp drains the TMEM lane quadrant w%4 of blocks w/4, w/4+NT/128, ...
+      float* base = a.pstage + (((size_t)grp * 2 + (t & 1)) * a.CL) * a.CL * N * a.UPC;
+      const int qd = w & 3;
+      for (int mb = w >> 2; mb < MB; mb += NT >> 7) {
+        const int c = mb * 128 + 32 * qd + l;
+        float v[16];
+        tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + mb * N, v);
+        if (c < DH) {
+          const int q = c / a.UPC, cu = c % a.UPC;
+          float* dst = base + (((size_t)q * a.CL + me) * N) * a.UPC + cu;
+#pragma unroll
+          for (int n = 0; n < N; ++n) dst[(size_t)n * a.UPC] = v[n];
+        }
+      }
+      fence_proxy_async_global();
+      tc_fence_before();
+      __syncthreads();
+      if (tid < a.CL) mbar_arrive_remote(mapa_shared(smem_u32(&bars[2 + (t & 1)]), tid));
+      FRNN_PROF(4, k);
+    }
+    // Off the critical path: dx (= dg for input-wired gates, engine.hpp:311-316).
+    if (valid) {
+      bf16* dxt = dx + (size_t)t * gstep + xo;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        if (p.inp[j]) st2(dxt, (size_t)j * D, dgv[j][0], dgv[j][1]);
+        else *reinterpret_cast<uint32_t*>(dxt + (size_t)j * D) = 0u;
+        if (a.dgw) st2(a.dgw + (size_t)t * gstep + xo, (size_t)j * D, dgv[j][0], dgv[j][1]);
+      }
+    }
+  }
+  if (recur && T > 0) absorb(0);
+  if (valid) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) st2(ds0, (size_t)s * B * D + so, ds[s][0], ds[s][1]);
+  }
+  if (a.dbacc) {  // db: fixed-order sum over the tile's batch rows (deterministic)
+    if (own) {
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        dbs[((size_t)j * N + b) * a.UPC + u] = dbv[j][0];
+        dbs[((size_t)j * N + b) * a.UPC + u + 1] = dbv[j][1];
+      }
+    }
+    __syncthreads();
+    const int tile = grp % a.NBT;
+    for (int q = tid; q < NG * a.UPC; q += NT) {
+      const int j = q / a.UPC, uu = q % a.UPC;
+      float sum = 0.f;
+      for (int bb = 0; bb < nb; ++bb) sum += dbs[((size_t)j * N + bb) * a.UPC + uu];
+      a.dbacc[((size_t)tile * NG + j) * D + hd * DH + unit0 + uu] = sum;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (w == 0) tmem_dealloc(tbase, a.tmem_cols);
+}
+
+uint32_t pow2_cols(uint32_t c) {
+  uint32_t r = 32;
+  while (r < c) r <<= 1;
+  return r;
+}
+
+int ngp_of(int NG) { return NG <= 1 ? 1 : NG <= 2 ? 2 : 4; }
+
+}  // namespace
+
+// ---------------------------------------------------------------- host ----
+ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
+  ClusterShape s{};
+  const int NGP = ngp_of(p.NG);
+  s.UPC = UPC;
+  s.CL = p.DH / UPC;
+  const int rows = UPC * NGP;
+  s.R1 = rows < 128 ? rows : 128;
+  s.R2 = rows - s.R1;
+  s.K = p.DH;
+  s.KBP = (rows + 15) / 16 * 16;
+  s.MB = (p.DH + 127) / 128;
+  s.slice = (uint32_t)UPC * N * 2;
+  const int NBT = (p.B + N - 1) / N;
+  s.groups = p.NH * NBT;
+  const int pairs = UPC / 2 * N;
+  s.threads = (int)align_up(pairs, 128);
+  s.EPT = pairs <= MAXT ? 1 : 0;  // one unit pair per thread (0 = unsupported)
+  if (!backward) {
+    s.acc1 = (uint32_t)align_up(s.K / 2, 32);
+    s.acc2 = s.acc1 + N;
+    s.tmem_cols = pow2_cols(s.acc2 + N);
+    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : 0) + (size_t)N * (rows + 1) * 4 +
+             align_up(s.slice, 16) + 64;
+    s.ws = align_up((size_t)s.groups * 2 * s.CL * s.slice, 256);
+  } else {
+    const int colblk = s.KBP / 2;
+    int mbt = (512 - s.MB * N) / colblk;
+    s.MBT = mbt < s.MB ? (mbt < 0 ? 0 : mbt) : s.MB;
+    s.acc1 = (uint32_t)(s.MBT * colblk);
+    s.tmem_cols = pow2_cols(s.acc1 + s.MB * N);
+    s.smem = (size_t)(s.MB - s.MBT) * 128 * s.KBP * 2 + (size_t)s.CL * N * UPC * 4 + (size_t)N * s.KBP * 2 +
+             (size_t)p.NG * N * UPC * 4 + 64;
+    s.ws = align_up((size_t)s.groups * 2 * s.CL * s.CL * N * UPC * 4, 256);
+  }
+  return s;
+}
+
+bool cluster_ept_supported(int ept) { return ept == 1; }
+
+namespace {
+
+CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, ClusterShape& cs) {
+  const int N = pl.batch_tile;
+  cs = cluster_shape(p, pl.units_per_cta, N, backward);
+  CArgs a{};
+  a.p = p;
+  a.UPC = cs.UPC;
+  a.CL = cs.CL;
+  a.NBT = (p.B + N - 1) / N;
+  a.R1 = cs.R1;
+  a.R2 = cs.R2;
+  a.K = cs.K;
+  a.KBP = cs.KBP;
+  a.MB = cs.MB;
+  a.MBT = cs.MBT;
+  a.tmem_cols = cs.tmem_cols;
+  a.acc1 = cs.acc1;
+  a.acc2 = cs.acc2;
+  a.slice = cs.slice;
+  a.prof = g_prof_buf;
+  a.prof_steps = g_prof_steps;
+  char* w = static_cast<char*>(ws);
+  if (!backward) {
+    a.xstage = reinterpret_cast<bf16*>(w);
+  } else {
+    a.pstage = reinterpret_cast<float*>(w);
+    size_t off = cs.ws;
+    bool all_in = true;
+    for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
+    if (!all_in) {
+      a.dgw = reinterpret_cast<bf16*>(w + off);
+      off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
+    }
+    a.dbacc = dr_gemm_supported(p) ? reinterpret_cast<float*>(w + off) : nullptr;
+  }
+  return a;
+}
+
+template <class KernelT>
+cudaError_t cluster_launch(KernelT kern, const CArgs& a, int grid, int threads, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (a.CL > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = a.CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <bool BWD>
+cudaError_t launch_variant(int variant, const CArgs& a, const ClusterShape& cs, cudaStream_t s) {
+  const int grid = cs.groups * cs.CL;
+  switch (variant) {
+    case kElman:
+      return cluster_launch(BWD ? cl_bwd_kernel<kElman, 16> : cl_fwd_kernel<kElman, 16>, a, grid, cs.threads, cs.smem, s);
+    case kLstm:
+      return cluster_launch(BWD ? cl_bwd_kernel<kLstm, 16> : cl_fwd_kernel<kLstm, 16>, a, grid, cs.threads, cs.smem, s);
+    case kGru:
+      return cluster_launch(BWD ? cl_bwd_kernel<kGru, 16> : cl_fwd_kernel<kGru, 16>, a, grid, cs.threads, cs.smem, s);
+    default:
+      return cluster_launch(BWD ? cl_bwd_kernel<kSlstm, 16> : cl_fwd_kernel<kSlstm, 16>, a, grid, cs.threads, cs.smem,
+                            s);
+  }
+}
+
+}  // namespace
+
+size_t cluster_forward_ws(const Problem& p, const Plan& pl) {
+  return cluster_shape(p, pl.units_per_cta, pl.batch_tile, false).ws;
+}
+
+size_t cluster_backward_ws(const Problem& p, const Plan& pl) {
+  size_t off = cluster_shape(p, pl.units_per_cta, pl.batch_tile, true).ws;
+  bool all_in = true;
+  for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
+  if (!all_in) off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
+  off += align_up(sizeof(float) * ((p.B + pl.batch_tile - 1) / pl.batch_tile) * p.NG * p.D, 256);  // db per tile
+  return off;
+}
+
+cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s) {
+  ClusterShape cs;
+  CArgs a = make_cargs(p, pl, ws, false, cs);
+  kt_begin(KT_FWD, s);
+  cudaError_t e = launch_variant<false>(p.variant, a, cs, s);
+  kt_end(KT_FWD, s);
+  return e;
+}
+
+cudaError_t cluster_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s) {
+  ClusterShape cs;
+  CArgs a = make_cargs(p, pl, ws, true, cs);
+  kt_begin(KT_BWD, s);
+  cudaError_t e = launch_variant<true>(p.variant, a, cs, s);
+  kt_end(KT_BWD, s);
+  if (e != cudaSuccess) return e;
+  const void* dgp = a.dgw ? static_cast<const void*>(a.dgw) : p.dx;
+  kt_begin(KT_PARAM, s);
+  if (a.dbacc) {
+    e = dr_gemm(p, dgp, s);
+    if (e == cudaSuccess) e = db_convert(a.dbacc, p.dbias, p.NG * p.D, a.NBT, s);
+  } else {
+    DgView dg{dgp, (long long)p.B * p.NG * p.D, (long long)p.NG * p.D, (long long)p.D};
+    e = param_grads(p, dg, nullptr, s);
+  }
+  kt_end(KT_PARAM, s);
+  return e;
+}
+
+}  // namespace frnn

@@ -33,6 +33,7 @@ struct Plan {
   int ctas_per_group;  // CTAs synchronising per step
   int groups;          // heads x batch tiles
   int grid, threads, smem_bytes, tmem_cols, k_split;
+  int cluster;         // >0: cluster-resident fused kernels with this cluster size
   size_t ws_bytes;
   double solve_us;
 };
@@ -52,6 +53,19 @@ size_t fused_forward_ws(const Problem& p, const Plan& pl);
 uint32_t fused_tmem_cols(const Problem& p, int N, bool backward);
 size_t fused_backward_ws(const Problem& p, const Plan& pl);
 
+// ---- cluster-resident fused path (fused_cluster.cu) ----
+struct ClusterShape {
+  int UPC, CL, R1, R2, K, KBP, MB, MBT, EPT, groups, threads;
+  uint32_t acc1, acc2, tmem_cols, slice;
+  size_t smem, ws;
+};
+ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward);
+bool cluster_ept_supported(int ept);
+cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+cudaError_t cluster_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
+size_t cluster_forward_ws(const Problem& p, const Plan& pl);
+size_t cluster_backward_ws(const Problem& p, const Plan& pl);
+
 // ---- alternating path (alternating.cu) ----
 cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
@@ -70,7 +84,8 @@ size_t param_grads_ws(const Problem& p);
 // ---- tcgen05 dR GEMM (dr_gemm.cu) ----
 bool dr_gemm_supported(const Problem& p);
 cudaError_t dr_gemm(const Problem& p, const void* dg_dx_layout, cudaStream_t s);
-cudaError_t db_convert(const float* acc, void* db, int n, cudaStream_t s);
+// db[i] = sum over batch tiles (fixed order) of acc[tile * n + i]
+cudaError_t db_convert(const float* acc, void* db, int n, int tiles, cudaStream_t s);
 
 // ---- utilities (util.cu) ----
 // Sets *flag (device int) to 1 if any of the n elements is non-finite.

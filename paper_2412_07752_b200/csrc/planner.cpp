@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/flashrnn.h"
@@ -83,6 +84,46 @@ static bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan
   return true;
 }
 
+// Cluster-resident fused kernels (fused_cluster.cu): largest units-per-CTA
+// (fewest CTAs in the cluster) whose slice fits TMEM (<=128 rows) + one M=64
+// SMEM block, with cluster size <= 16 and SMEM/TMEM within the device limits.
+static bool plan_cluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
+  const int NGP = ngp_of(p.NG);
+  const int N = 16;
+  if (p.DH % 16 || p.DH > 960) {
+    *why = "cluster: head_dim must be a multiple of 16 and <= 960";
+    return false;
+  }
+  for (int upc : {48, 32, 16, 8}) {
+    if (p.DH % upc) continue;
+    const int rows = upc * NGP, CL = p.DH / upc;
+    if (rows > 192 || CL > 16) continue;
+    ClusterShape cf = cluster_shape(p, upc, N, false), cb = cluster_shape(p, upc, N, true);
+    if (!cluster_ept_supported(cf.EPT)) continue;
+    const ClusterShape& cs = pass == 0 ? cf : cb;
+    if ((int)cs.tmem_cols > lim.tmem_cols || (int)cs.smem > lim.smem_optin) continue;
+    if (pass == 1 && cb.MBT < 1) continue;
+    Plan& pl = *out;
+    pl = Plan{};
+    pl.algo = FRNN_ALGO_FUSED;
+    pl.cluster = CL;
+    pl.rows_per_cta = rows;
+    pl.batch_tile = N;
+    pl.units_per_cta = upc;
+    pl.ctas_per_group = CL;
+    pl.groups = cs.groups;
+    pl.grid = cs.groups * CL;
+    pl.threads = cs.threads;
+    pl.smem_bytes = (int)cs.smem;
+    pl.tmem_cols = (int)cs.tmem_cols;
+    pl.k_split = 1;
+    pl.ws_bytes = pass == 0 ? cluster_forward_ws(p, pl) : cluster_backward_ws(p, pl);
+    return true;
+  }
+  *why = "cluster: no units-per-CTA fits (cluster <= 16, rows <= 192)";
+  return false;
+}
+
 static bool plan_simt(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
   const size_t smem = simt_smem_bytes(p, pass == 1);
   if ((int)smem > lim.smem_optin) {
@@ -119,6 +160,7 @@ int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Pl
     return FRNN_EUNSUPPORTED;
   }
   if (algo == FRNN_ALGO_AUTO || algo == FRNN_ALGO_FUSED) {
+    if (!getenv("FRNN_NO_CLUSTER") && plan_cluster(p, pass, lim, out, why)) return FRNN_OK;
     if (plan_fused(p, pass, lim, out, why)) return FRNN_OK;
     if (algo == FRNN_ALGO_FUSED) return FRNN_EINFEASIBLE;
   }

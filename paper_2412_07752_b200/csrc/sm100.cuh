@@ -102,6 +102,64 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// Whole-warp MMA chains in one PTX loop: every lane runs the loop on uniform
+// registers (so ptxas keeps them in the uniform datapath) and elect.sync guards
+// only the tcgen05.mma.  Iteration k issues
+//   D[d] (+)= A . B   with A = a0 + k*a_step (TMEM address or smem descriptor),
+//   B desc = b0 + k*b_step, accumulate = (k > 0 || acc_first).
+// Must be called by all 32 lanes of one warp.
+__device__ __forceinline__ void mma_chain_ts(uint32_t d, uint32_t a0, uint32_t a_step, uint64_t b0, uint64_t b_step,
+                                             uint32_t idesc, int n) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 k, ta;\n\t.reg .b64 bd;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 k, 0;\n\tmov.b32 ta, %1;\n\tmov.b64 bd, %3;\n\t"
+      "setp.ge.s32 q, k, %6;\n\t@q bra.uni CHTS_END%=;\n\t"
+      "CHTS_LOOP%=:\n\t"
+      "setp.ne.b32 p, k, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %5, p;\n\t"
+      "add.u32 ta, ta, %2;\n\tadd.u64 bd, bd, %4;\n\tadd.s32 k, k, 1;\n\t"
+      "setp.lt.s32 q, k, %6;\n\t@q bra.uni CHTS_LOOP%=;\n\t"
+      "CHTS_END%=:\n\t}" ::"r"(d),
+      "r"(a0), "r"(a_step), "l"(b0), "l"(b_step), "r"(idesc), "r"(n)
+      : "memory");
+}
+__device__ __forceinline__ void mma_chain_ss(uint32_t d, uint64_t a0, uint64_t a_step, uint64_t b0, uint64_t b_step,
+                                             uint32_t idesc, int n) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 k;\n\t.reg .b64 ad, bd;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 k, 0;\n\tmov.b64 ad, %1;\n\tmov.b64 bd, %3;\n\t"
+      "setp.ge.s32 q, k, %6;\n\t@q bra.uni CHSS_END%=;\n\t"
+      "CHSS_LOOP%=:\n\t"
+      "setp.ne.b32 p, k, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %5, p;\n\t"
+      "add.u64 ad, ad, %2;\n\tadd.u64 bd, bd, %4;\n\tadd.s32 k, k, 1;\n\t"
+      "setp.lt.s32 q, k, %6;\n\t@q bra.uni CHSS_LOOP%=;\n\t"
+      "CHSS_END%=:\n\t}" ::"r"(d),
+      "l"(a0), "l"(a_step), "l"(b0), "l"(b_step), "r"(idesc), "r"(n)
+      : "memory");
+}
+// Interleaved pair chain: TS (M=128) into d1 and SS into d2 sharing B.
+__device__ __forceinline__ void mma_chain_ts_ss(uint32_t d1, uint32_t a1, uint32_t a1_step, uint32_t d2, uint64_t a2,
+                                                uint64_t a2_step, uint64_t b0, uint64_t b_step, uint32_t idesc1,
+                                                uint32_t idesc2, int n) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 k, ta;\n\t.reg .b64 ad, bd;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 k, 0;\n\tmov.b32 ta, %1;\n\tmov.b64 ad, %4;\n\tmov.b64 bd, %6;\n\t"
+      "setp.ge.s32 q, k, %10;\n\t@q bra.uni CHP_END%=;\n\t"
+      "CHP_LOOP%=:\n\t"
+      "setp.ne.b32 p, k, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bd, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], ad, bd, %9, p;\n\t"
+      "add.u32 ta, ta, %2;\n\tadd.u64 ad, ad, %5;\n\tadd.u64 bd, bd, %7;\n\tadd.s32 k, k, 1;\n\t"
+      "setp.lt.s32 q, k, %10;\n\t@q bra.uni CHP_LOOP%=;\n\t"
+      "CHP_END%=:\n\t}" ::"r"(d1),
+      "r"(a1), "r"(a1_step), "r"(d2), "l"(a2), "l"(a2_step), "l"(b0), "l"(b_step), "r"(idesc1), "r"(idesc2), "r"(n)
+      : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05.mma complete.
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
   asm volatile(
@@ -117,14 +175,34 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t a = smem_u32(bar);
+__device__ __forceinline__ uint64_t globaltimer_ns();
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t phase) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(a),
-      "r"(phase)
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_cluster(uint32_t a, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, "
+      "1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// try_wait suspends in hardware; after ~4 s without completion the kernel
+// traps (a protocol bug must not hang the GPU).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try(a, phase)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try(a, phase))
+    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -189,6 +267,54 @@ __device__ __forceinline__ float4 ld_cg_f4(const void* p) {
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
   return r;
+}
+
+// ------------------------------------------------------------- clusters ---
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+// Full cluster barrier (all threads of all CTAs), release/acquire at cluster scope.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared-memory location in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// Wait on a local mbarrier whose arrivals/transactions come from other CTAs.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_cluster(a, phase)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_cluster(a, phase))
+    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+}
+// Arrive (count 1) on the mbarrier at cluster-shared address `remote`.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// Generic-proxy global writes -> visible to the async proxy (TMA reads).
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// TMA bulk load global -> the same smem offset in every CTA of ctaMask,
+// complete_tx on each destination's mbarrier at the same offset.
+__device__ __forceinline__ void bulk_g2s_multicast(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
