@@ -8,6 +8,7 @@
  * frnn_debug_timing / frnn_debug_kernel_ms: CUDA-event timing of each kernel
  *   class on its launch stream -- [0] forward recurrence, [1] backward
  *   recurrence, [2] dR/db reduction -- summed in ms with launch counts.
+ * frnn_debug_launches: total kernels the library has launched since load.
  */
 #ifndef FLASHRNN_DEBUG_H_
 #define FLASHRNN_DEBUG_H_
@@ -18,6 +19,7 @@ extern "C" {
 FRNN_API int frnn_debug_profile(void* device_buffer, int32_t steps);
 FRNN_API int frnn_debug_timing(int32_t enable);
 FRNN_API int frnn_debug_kernel_ms(double* ms3, int64_t* count3);
+FRNN_API int frnn_debug_launches(int64_t* count);
 #ifdef __cplusplus
 }
 #endif

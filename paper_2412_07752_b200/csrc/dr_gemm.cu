@@ -223,11 +223,13 @@ cudaError_t dr_gemm(const Problem& p, const void* dg, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   dim3 grid(p.NG * p.DH / BM, p.DH / BN, p.NH);
   dr_gemm_kernel<<<grid, 128, smem, s>>>(ma, mb, g);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t db_convert(const float* acc, void* db, int n, int tiles, cudaStream_t s) {
   db_convert_kernel<<<(n + 255) / 256, 256, 0, s>>>(acc, static_cast<bf16*>(db), n, tiles);
+  note_launch();
   return cudaGetLastError();
 }
 

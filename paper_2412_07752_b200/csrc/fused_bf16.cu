@@ -633,6 +633,7 @@ cudaError_t coop_launch(KernelT kern, const FArgs& a, int grid, size_t smem, cud
   if (e != cudaSuccess) return e;
   FArgs copy = a;
   void* args[] = {&copy};
+  note_launch();
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(128), args, smem,
                                      s);
 }

@@ -668,6 +668,7 @@ cudaError_t cluster_launch(KernelT kern, const CArgs& a, int grid, int threads, 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  note_launch();
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

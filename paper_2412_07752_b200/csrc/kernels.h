@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstddef>
 #include <cstdint>
+#include <string>
 
 namespace frnn {
 
@@ -67,6 +68,19 @@ size_t cluster_forward_ws(const Problem& p, const Plan& pl);
 size_t cluster_backward_ws(const Problem& p, const Plan& pl);
 
 // ---- alternating path (alternating.cu) ----
+struct AltShape {
+  int N, NBT;            // batch tile (MMA N) and batch tiles
+  int UPT;               // forward: hidden units per CTA (128 / NG gate rows each)
+  int tiles;             // forward: unit tiles; backward: 128-column tiles
+  int numk;              // K blocks (of 64) per CTA
+  int KS, KT, kpg, nrec; // backward: cluster K split, K blocks, blocks per gate, R-gates
+  int recg[4];
+  int stages, grid, ka;  // ka: 64-wide K atoms per stage
+  uint32_t stage_bytes, a_bytes, region, tmem_cols;
+  size_t smem;
+};
+AltShape alt_shape(const Problem& p, bool backward, int sm_count);
+bool alt_supported(const Problem& p, std::string* why);
 cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 size_t alt_forward_ws(const Problem& p, const Plan& pl);
@@ -92,6 +106,9 @@ cudaError_t db_convert(const float* acc, void* db, int n, int tiles, cudaStream_
 cudaError_t check_finite(const void* ptr, size_t n, bool bf16, int* flag, cudaStream_t s);
 
 int sm_count();
+
+// Counts every kernel this library launches (frnn_debug_launches).
+void note_launch(int n = 1);
 
 // ---- optional per-kernel-class event timing (ktimer.cpp) ----
 enum KernelClass { KT_FWD = 0, KT_BWD = 1, KT_PARAM = 2, KT_N = 3 };

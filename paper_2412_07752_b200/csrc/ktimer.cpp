@@ -3,6 +3,7 @@
 // launch stream).  Disabled by default: kt_begin/kt_end are then no-ops.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -33,7 +34,11 @@ cudaEvent_t take() {
   return e;
 }
 
+std::atomic<long long> g_launches{0};
+
 }  // namespace
+
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void kt_begin(int cls, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -79,6 +84,12 @@ int frnn_debug_kernel_ms(double* ms3, int64_t* count3) {
     frnn::g_pool.push_back(sp.e);
   }
   frnn::g_spans.clear();
+  return FRNN_OK;
+}
+
+// Total kernels launched by the library since load (bench.py gpu_launches).
+int frnn_debug_launches(int64_t* count) {
+  if (count) *count = frnn::g_launches.load();
   return FRNN_OK;
 }
 

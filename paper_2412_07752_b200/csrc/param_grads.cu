@@ -107,6 +107,7 @@ cudaError_t param_grads(const Problem& p, DgView dg, void*, cudaStream_t s) {
     dr_db_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p, dg);
   else
     dr_db_kernel<float><<<grid, 256, 0, s>>>(p, dg);
+  note_launch();
   return cudaGetLastError();
 }
 

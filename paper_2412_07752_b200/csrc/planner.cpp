@@ -164,9 +164,30 @@ int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Pl
     if (plan_fused(p, pass, lim, out, why)) return FRNN_OK;
     if (algo == FRNN_ALGO_FUSED) return FRNN_EINFEASIBLE;
   }
+  std::string alt_why;
+  if (!alt_supported(p, &alt_why)) {
+    *why = why->empty() ? alt_why : *why + "; " + alt_why;
+    return FRNN_EINFEASIBLE;
+  }
+  const AltShape sh = alt_shape(p, pass == 1, lim.sm_count);
+  if ((int)sh.smem > lim.smem_optin) {
+    *why = "alternating path: shared memory";
+    return FRNN_EINFEASIBLE;
+  }
   Plan& pl = *out;
   pl = Plan{};
   pl.algo = FRNN_ALGO_ALTERNATING;
+  pl.rows_per_cta = 128;
+  pl.batch_tile = sh.N;
+  pl.units_per_cta = pass == 0 ? sh.UPT : 128 / sh.KS;
+  pl.ctas_per_group = sh.KS;
+  pl.groups = sh.tiles * p.NH * sh.NBT;
+  pl.grid = sh.grid;
+  pl.threads = 256;
+  pl.smem_bytes = (int)sh.smem;
+  pl.tmem_cols = (int)sh.tmem_cols;
+  pl.k_split = sh.KS;
+  pl.cluster = sh.KS > 1 ? sh.KS : 0;
   pl.ws_bytes = pass == 0 ? alt_forward_ws(p, pl) : alt_backward_ws(p, pl);
   return FRNN_OK;
 }

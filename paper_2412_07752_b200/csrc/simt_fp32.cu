@@ -203,7 +203,7 @@ cudaError_t simt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_
   {                                                                                       \
     e = cudaFuncSetAttribute(simt_fwd_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)smem);                                                  \
-    if (e == cudaSuccess) simt_fwd_kernel<V><<<grid, THREADS, smem, s>>>(p);              \
+    if (e == cudaSuccess) simt_fwd_kernel<V><<<grid, THREADS, smem, s>>>(p), note_launch(); \
   }
   switch (p.variant) {
     case kElman: LAUNCH_F(kElman); break;
@@ -225,7 +225,7 @@ cudaError_t simt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream
   {                                                                                       \
     e = cudaFuncSetAttribute(simt_bwd_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)smem);                                                  \
-    if (e == cudaSuccess) simt_bwd_kernel<V><<<grid, THREADS, smem, s>>>(p, dgw);         \
+    if (e == cudaSuccess) simt_bwd_kernel<V><<<grid, THREADS, smem, s>>>(p, dgw), note_launch(); \
   }
   switch (p.variant) {
     case kElman: LAUNCH_B(kElman); break;

@@ -31,6 +31,7 @@ cudaError_t check_finite(const void* ptr, size_t n, bool bf16, int* flag, cudaSt
     finite_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(ptr), n, flag);
   else
     finite_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(ptr), n, flag);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -76,8 +76,8 @@ def assert_close(gpu, ora, tol, keys=("states", "gates", "dx", "dbias", "dR", "d
     return errs
 
 
-def check_bf16(eng, orc, v, inp, clip="off", mag=0.0, dh=None):
-    gpu = run_gpu(eng, v, inp, True, clip, mag, dh)
+def check_bf16(eng, orc, v, inp, clip="off", mag=0.0, dh=None, algo="auto"):
+    gpu = run_gpu(eng, v, inp, True, clip, mag, dh, algo)
     ora = run_oracle(orc, v, inp, True, clip, mag, dh)
     fwd = assert_close(gpu, ora, BF16_TOL, ("states", "gates"))
     r = {k: orc.round_bf16(inp[k]) for k in ("R", "dsf")}
@@ -184,6 +184,74 @@ def test_bf16_golden(eng, orc):
     for v in VARIANTS:
         g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", f"{v}_small.npz")))
         check_bf16(eng, orc, v, {k: g[k] for k in ("R", "bias", "x", "s0", "dsf")})
+
+
+# ------------------------------------------- alternating path (K4/K5) ----
+@pytest.mark.parametrize("v", VARIANTS)
+def test_alternating_variants(eng, orc, v):
+    """Per-step streamed-R kernels (forced), two heads, ragged batch tile."""
+    inp = orc.generate(v, 12, 21, 2, 128, seed=3)
+    check_bf16(eng, orc, v, inp, algo="alternating")
+
+
+@pytest.mark.parametrize("v", VARIANTS)
+@pytest.mark.parametrize("clip,mag", [("value", 0.05), ("zero", 0.0)])
+def test_alternating_clip_and_step_grads(eng, orc, v, clip, mag):
+    inp = orc.generate(v, 8, 16, 1, 192, seed=4)
+    dh = np.random.RandomState(3).randn(8, 16, 192)
+    check_bf16(eng, orc, v, inp, clip, mag, dh=dh, algo="alternating")
+
+
+def test_alternating_two_batch_tiles(eng, orc):
+    """B=160: batch tiles of 128 (the second ragged), per-tile db partials."""
+    inp = orc.generate("lstm", 6, 160, 1, 128, seed=7)
+    check_bf16(eng, orc, "lstm", inp, algo="alternating")
+
+
+def test_alternating_matches_fused(eng, orc):
+    """Same inputs through the cluster-resident and the alternating kernels."""
+    inp = orc.generate("slstm", 16, 16, 1, 768, seed=8)
+    a = run_gpu(eng, "slstm", inp, True, algo="fused")
+    b = run_gpu(eng, "slstm", inp, True, algo="alternating")
+    assert_close(b, a, BF16_TOL, ("states", "gates"))
+
+
+def test_config5_slstm_h3072(eng, orc):
+    """BASELINE config 5 shape: sLSTM H=3072, B=64, NH=1 (R = 75.5 MB, beyond
+    on-chip capacity -> the planner picks the alternating path); T=3 (oracle cost)."""
+    p = eng.plan("slstm", 3, 64, 1, 3072, "bf16", "backward")
+    assert p["algo"] == 2, p
+    inp = orc.generate("slstm", 3, 64, 1, 3072, seed=0)
+    check_bf16(eng, orc, "slstm", inp)
+
+
+def test_config5_full_size_properties(eng, orc):
+    """sLSTM H=3072, B=64, T=1024: deterministic, finite, causal prefix parity."""
+    import torch
+    T, B, DH, NS, NG = 1024, 64, 3072, 4, 4
+    g = torch.Generator(device="cuda").manual_seed(0)
+    R = (torch.randn(1, NG, DH, DH, device="cuda", generator=g) / DH ** 0.5).bfloat16()
+    b = (0.1 * torch.randn(NG, DH, device="cuda", generator=g)).bfloat16()
+    x = torch.randn(T, B, NG, DH, device="cuda", generator=g).bfloat16()
+    s0 = 0.5 * torch.randn(NS, B, DH, device="cuda", generator=g)
+    s0[2] = 1 + 0.1 * s0[2].abs()
+    s0[3] = 0
+    s0 = s0.bfloat16()
+    dsf = torch.randn(NS, B, DH, device="cuda", generator=g).bfloat16()
+    st1, ga1 = eng.forward("slstm", R, b, x, s0)
+    gr1 = eng.backward("slstm", R, b, st1, ga1, dsf)
+    st2, ga2 = eng.forward("slstm", R, b, x, s0)
+    gr2 = eng.backward("slstm", R, b, st2, ga2, dsf)
+    torch.cuda.synchronize()
+    assert torch.equal(st1, st2) and torch.equal(ga1, ga2)
+    for k in gr1:
+        assert torch.equal(gr1[k], gr2[k]), k
+        assert torch.isfinite(gr1[k].float()).all(), k
+    assert torch.isfinite(st1.float()).all()
+    P = 2
+    ost, oga = orc.forward("slstm", _np(R), _np(b), _np(x[:P]), _np(s0))
+    assert normwise(_np(st1[: P + 1]), ost) <= BF16_TOL
+    assert normwise(_np(ga1[:P]), oga) <= BF16_TOL
 
 
 # ---------------------------------------------- full-size property tests ----
