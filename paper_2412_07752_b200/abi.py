@@ -65,7 +65,7 @@ class Shard(C.Structure):
 
 
 EXPORTS = ["frnn_version", "frnn_last_error", "frnn_cell_spec", "frnn_plan", "frnn_workspace_size",
-           "frnn_forward", "frnn_backward", "frnn_partition"]
+           "frnn_forward", "frnn_backward", "frnn_partition", "frnn_csp_solve", "frnn_csp_brute_force"]
 
 
 def lib_path() -> str:
@@ -221,6 +221,40 @@ class FlashRNN:
             out["dx"].data_ptr(), out["dbias"].data_ptr(), out["dR"].data_ptr(),
             out["ds0"].data_ptr(), ws.data_ptr(), ws.numel(), C.byref(o), s))
         return out
+
+
+def csp_solve(problem: str) -> tuple[dict | None, dict]:
+    """The tiling solver's CSP engine (include/flashrnn_csp.h) on a problem in
+    text form -> ({id: value} or None when infeasible, stats)."""
+    L = load()
+    L.frnn_csp_solve.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64)]
+    L.frnn_csp_solve.restype = C.c_int
+    buf = C.create_string_buffer(1 << 20)
+    st = (C.c_int64 * 3)()
+    rc = L.frnn_csp_solve(problem.encode(), buf, len(buf), st)
+    stats = {"nodes": st[0], "backtracks": st[1], "solve_us": st[2] / 1e3}
+    if rc == 4:
+        return None, stats
+    _check(rc)
+    return _parse_assignment(buf.value.decode()), stats
+
+
+def csp_brute_force(problem: str, cap: int = 1 << 22) -> list[dict]:
+    L = load()
+    L.frnn_csp_brute_force.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64)]
+    L.frnn_csp_brute_force.restype = C.c_int
+    buf = C.create_string_buffer(1 << 24)
+    n = C.c_int64()
+    _check(L.frnn_csp_brute_force(problem.encode(), cap, buf, len(buf), C.byref(n)))
+    return [_parse_assignment(b) for b in buf.value.decode().split("--\n") if b.strip()]
+
+
+def _parse_assignment(text: str) -> dict:
+    out = {}
+    for line in text.strip().splitlines():
+        k, v = line.split("=")
+        out[k] = int(v)
+    return out
 
 
 def partition(T, B, NH, DH, world_size: int, rank: int) -> dict:

@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     syms = set()
-    for h in ("flashrnn.h", "flashrnn_debug.h"):
+    for h in sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h")):
         text = open(os.path.join(ROOT, "include", h)).read()
         syms |= set(re.findall(r"FRNN_API\s+[\w\s\*]*?\b(frnn_\w+)\s*\(", text))
     return syms
