@@ -48,7 +48,7 @@ NGREC = {"elman": 1, "lstm": 4, "gru": 3, "slstm": 4}
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--variant", default="slstm", choices=list(NS_NG))
@@ -61,9 +61,10 @@ def parse():
     return ap.parse_args()
 
 
-def workload_name(a):
+def workload_name(a, algo=None):
+    path = {1: " (fused kernel, R resident on-chip)", 2: " (alternating path, R streamed from L2 every step)"}
     return (f"{a.variant} fwd+bwd bf16, B={a.batch}/GPU, T={a.seq}, H={a.hidden}, NH={a.heads}"
-            + (" (fused kernel, R resident on-chip)" if a.hidden // a.heads <= 768 else ""))
+            + path.get(algo, ""))
 
 
 def flops_per_pass(a):
@@ -96,7 +97,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
@@ -267,6 +268,7 @@ def run_ours(a, rank, world, local_rank):
     eng = FlashRNN()
     L = load()
     L.frnn_debug_timing.argtypes = [C.c_int32]
+    L.frnn_debug_launches.argtypes = [C.POINTER(C.c_int64)]
     L.frnn_debug_kernel_ms.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     shard = partition(a.seq, a.batch * world, a.heads, a.hidden // a.heads, world, rank)
     inp = make_inputs(torch, dev, a, seed=rank)
@@ -294,6 +296,8 @@ def run_ours(a, rank, world, local_rank):
     clocks = ClockSampler(local_rank)
     clocks.start()
     L.frnn_debug_timing(1)
+    launches0 = C.c_int64()
+    L.frnn_debug_launches(C.byref(launches0))
     L.frnn_debug_kernel_ms(None, None)  # clear
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     if world > 1:
@@ -311,6 +315,8 @@ def run_ours(a, rank, world, local_rank):
     cnt3 = (C.c_int64 * 3)()
     L.frnn_debug_kernel_ms(ms3, cnt3)
     L.frnn_debug_timing(0)
+    launches1 = C.c_int64()
+    L.frnn_debug_launches(C.byref(launches1))
     clk = clocks.stop()
     total_ms = sum(s.elapsed_time(e) for s, e in ev)
     if world > 1:
@@ -322,8 +328,15 @@ def run_ours(a, rank, world, local_rank):
     value = units / (ms_step / 1e3)
 
     # ---- roofline of the dominant kernel (live CUDA-event timing) ----
-    names = ["forward recurrence (fused_fwd_kernel)", "backward recurrence (fused_bwd_kernel)",
-             "dR/db reduction (dr_db_kernel)"]
+    plan = {p: eng.plan(a.variant, a.seq, a.batch, a.heads, a.hidden // a.heads, "bf16", p)
+            for p in ("forward", "backward")}
+    if plan["forward"]["algo"] == 2:
+        names = [f"forward recurrence (alt_fwd_kernel, {a.seq} PDL-chained launches)",
+                 f"backward recurrence (alt_bwd_kernel, {a.seq + 1} launches, cluster split-K)",
+                 "dR GEMM + db (dr_gemm_kernel, db_convert_kernel)"]
+    else:
+        names = ["forward recurrence (cl_fwd_kernel)", "backward recurrence (cl_bwd_kernel)",
+                 "dR GEMM + db (dr_gemm_kernel, db_convert_kernel)"]
     shares = [ms3[i] for i in range(3)]
     dom = max(range(3), key=lambda i: shares[i])
     peaks, peak_src = measured_peaks()
@@ -345,6 +358,17 @@ def run_ours(a, rank, world, local_rank):
                                     "backward": 1e3 * ms3[1] / max(1, cnt3[1]) / a.seq},
             "kernel_ms_per_step": {"forward": ms3[0] / a.steps, "backward": ms3[1] / a.steps,
                                    "param_grads": ms3[2] / a.steps}}
+    if plan["forward"]["algo"] == 2 and dom < 2:
+        # alternating path: R (beyond on-chip capacity) is streamed
+        # from L2/HBM every step; its byte rate against the measured HBM copy peak
+        ns_, ng_ = NS_NG[a.variant]
+        dh = a.hidden // a.heads
+        r_bytes = 2.0 * a.heads * ng_ * dh * dh
+        gbs = r_bytes * a.seq / (avg_ms / 1e3) / 1e9
+        hbm = peaks.get("hbm_gbs", 6533.0)
+        roof["r_stream"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                            "bytes_per_launch": r_bytes * a.seq,
+                            "note": "R re-read every step (served mostly from L2); HBM copy peak as denominator"}
 
     # ---- end to end through the C ABI with host buffers ----
     host = {k: v.cpu().pin_memory() for k, v in inp.items()}
@@ -384,20 +408,18 @@ def run_ours(a, rank, world, local_rank):
 
     if rank != 0:
         return
-    plan = {p: eng.plan(a.variant, a.seq, a.batch, a.heads, a.hidden // a.heads, "bf16", p)
-            for p in ("forward", "backward")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (torch RNG on device, reference generator distributions)",
-        "config": {"workload": workload_name(a), "variant": a.variant, "batch_per_gpu": a.batch,
+        "config": {"workload": workload_name(a, plan["forward"]["algo"]), "variant": a.variant, "batch_per_gpu": a.batch,
                    "global_batch": a.batch * world, "seq_len": a.seq, "hidden": a.hidden, "heads": a.heads,
                    "parallelism": f"batch-shard x{world} (frnn_partition: {shard})" if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MB write, outside the events)"},
         "roofline": roof,
         "e2e": e2e,
-        "gpu_launches": int(sum(cnt3[i] for i in range(3))),
+        "gpu_launches": int(launches1.value - launches0.value),
         "clocks": clk,
         "plan": {k: {kk: v[kk] for kk in ("algo", "grid", "ctas_per_group", "units_per_cta", "tmem_cols",
                                           "smem_bytes", "solve_us") if kk in v}

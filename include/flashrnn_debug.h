@@ -12,6 +12,8 @@
  */
 #ifndef FLASHRNN_DEBUG_H_
 #define FLASHRNN_DEBUG_H_
+#include <stddef.h>
+
 #include "flashrnn.h"
 #ifdef __cplusplus
 extern "C" {
@@ -20,6 +22,10 @@ FRNN_API int frnn_debug_profile(void* device_buffer, int32_t steps);
 FRNN_API int frnn_debug_timing(int32_t enable);
 FRNN_API int frnn_debug_kernel_ms(double* ms3, int64_t* count3);
 FRNN_API int frnn_debug_launches(int64_t* count);
+/* The planner's tiling CSP (algo FRNN_ALGO_FUSED = cluster-resident kernels,
+ * FRNN_ALGO_ALTERNATING) for a shape, in the text form of flashrnn_csp.h. */
+FRNN_API int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                                 int32_t algo, char* out, size_t out_bytes);
 #ifdef __cplusplus
 }
 #endif

@@ -154,11 +154,7 @@ class FlashRNN:
         return buf
 
     def plan(self, variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto") -> dict:
-        info = PlanInfo()
-        o = self._opts(algo)
-        _check(self.lib.frnn_plan(C.byref(cell_spec(variant)), Shape(T, B, NH, DH), DTYPE[dtype],
-                                  PASS[pass_], C.byref(o), C.byref(info)))
-        return info.as_dict()
+        return plan(variant, T, B, NH, DH, dtype, pass_, algo)
 
     def workspace_size(self, variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto"):
         n = C.c_size_t()
@@ -221,6 +217,15 @@ class FlashRNN:
             out["dx"].data_ptr(), out["dbias"].data_ptr(), out["dR"].data_ptr(),
             out["ds0"].data_ptr(), ws.data_ptr(), ws.numel(), C.byref(o), s))
         return out
+
+
+def plan(variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto") -> dict:
+    """frnn_plan: the tiling the solver picks for one pass (no GPU needed)."""
+    info = PlanInfo()
+    o = Options(0, ALGO[algo])
+    _check(load().frnn_plan(C.byref(cell_spec(variant)), Shape(T, B, NH, DH), DTYPE[dtype], PASS[pass_],
+                            C.byref(o), C.byref(info)))
+    return info.as_dict()
 
 
 def csp_solve(problem: str) -> tuple[dict | None, dict]:

@@ -311,6 +311,21 @@ int frnn_partition(frnn_shape shape, int32_t world_size, int32_t rank, frnn_shar
   return FRNN_OK;
 }
 
+int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass, int32_t algo,
+                        char* out, size_t out_bytes) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  try {
+    const std::string t = frnn::plan_csp_text(make_problem(cell, shape, dtype), pass, algo, frnn::device_limits());
+    if (!out || t.size() + 1 > out_bytes) return fail(FRNN_EINVAL_ARG, "output buffer too small");
+    std::memcpy(out, t.c_str(), t.size() + 1);
+    return FRNN_OK;
+  } catch (const std::exception& e) {
+    return fail(FRNN_EINVAL_ARG, e.what());
+  }
+}
+
 int frnn_debug_profile(void* device_buffer, int32_t steps) {
   frnn::g_prof_buf = static_cast<long long*>(device_buffer);
   frnn::g_prof_steps = device_buffer ? steps : 0;

@@ -641,46 +641,38 @@ StepKernel pick(int variant, bool bwd) {
 
 }  // namespace
 
-AltShape alt_shape(const Problem& p, bool backward, int sm_count) {
+// Derived geometry of one alternating pass for the solver's choices (planner.cpp):
+// batch tile N, backward cluster K-split KS, K atoms per stage ka, ring stages.
+AltShape alt_shape(const Problem& p, bool backward, int N, int KS, int ka, int stages) {
   AltShape s{};
-  s.N = std::min(128, (p.B + 15) / 16 * 16);
-  s.NBT = (p.B + s.N - 1) / s.N;
-  const char* kenv = getenv("FRNN_ALT_KA");  // experiment hook
-  s.ka = kenv ? atoi(kenv) : (p.DH % 128 == 0 ? 2 : 1);
-  if (s.ka < 1 || p.DH % (64 * s.ka)) s.ka = 1;
-  s.a_bytes = A_BYTES * s.ka;
-  s.stage_bytes = s.ka * (A_BYTES + (uint32_t)s.N * 128);
-  s.kpg = p.DH / (64 * s.ka);
+  s.N = N;
+  s.NBT = (p.B + N - 1) / N;
+  s.ka = ka;
+  s.a_bytes = A_BYTES * ka;
+  s.stage_bytes = ka * (A_BYTES + (uint32_t)N * 128);
+  s.kpg = p.DH / (64 * ka);
   size_t epi;
   if (!backward) {
     s.UPT = p.NG == 1 ? 128 : 32;
     s.tiles = (p.DH + s.UPT - 1) / s.UPT;
     s.numk = s.kpg;
     s.KS = 1;
-    epi = (size_t)128 * (s.N + 1) * 4;
+    epi = (size_t)128 * (N + 1) * 4;
   } else {
     s.tiles = (p.DH + 127) / 128;
     s.nrec = 0;
     for (int j = 0; j < p.NG; ++j)
       if (p.rec[j]) s.recg[s.nrec++] = j;
     s.KT = s.nrec * s.kpg;
-    const int base = s.tiles * p.NH * s.NBT;
-    int ks = sm_count / std::max(1, base);
-    ks = std::max(1, std::min({ks, MAXKS, std::max(1, s.KT)}));
-    if (s.nrec == 0) ks = 1;
-    s.KS = ks;
-    s.numk = (s.KT + ks - 1) / ks;
-    epi = (size_t)s.N * PC * 4;
+    s.KS = KS;
+    s.numk = (s.KT + KS - 1) / KS;
+    epi = (size_t)N * PC * 4;
   }
-  const char* env = getenv("FRNN_ALT_SMEM_KB");  // experiment hook: ring budget
-  const uint32_t budget = (env ? (uint32_t)atoi(env) : 200u) * 1024u;
-  int st = (int)((budget - 2048) / s.stage_bytes);
-  st = std::max(2, std::min({st, 8, std::max(2, s.numk)}));
-  s.stages = st;
-  s.region = (uint32_t)std::max<size_t>((size_t)st * s.stage_bytes, epi);
+  s.stages = stages;
+  s.region = (uint32_t)std::max<size_t>((size_t)stages * s.stage_bytes, epi);
   s.region = (s.region + 1023) & ~1023u;
   s.smem = 1024 + s.region + 256;
-  s.tmem_cols = pow2_at_least((uint32_t)s.N, 32);
+  s.tmem_cols = pow2_at_least((uint32_t)N, 32);
   s.grid = (backward ? s.tiles * s.KS : s.tiles) * p.NH * s.NBT;
   return s;
 }
@@ -714,7 +706,7 @@ size_t alt_backward_ws(const Problem& p, const Plan& pl) {
 cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t st) {
   std::string why;
   if (!alt_supported(p, &why) || !tmap_encoder()) return cudaErrorNotSupported;
-  const AltShape sh = alt_shape(p, false, sm_count());
+  const AltShape sh = alt_shape(p, false, pl.batch_tile, 1, pl.ka, pl.stages);
   CUtensorMap mR, mH;
   {  // R[NH][NG][DH][DH]: (k, unit, gate, head), box = (64, UPT, NG, 1)
     cuuint64_t dims[4] = {(cuuint64_t)p.DH, (cuuint64_t)p.DH, (cuuint64_t)p.NG, (cuuint64_t)p.NH};
@@ -766,7 +758,7 @@ cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t
 cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t st) {
   std::string why;
   if (!alt_supported(p, &why) || !tmap_encoder()) return cudaErrorNotSupported;
-  const AltShape sh = alt_shape(p, true, sm_count());
+  const AltShape sh = alt_shape(p, true, pl.batch_tile, pl.k_split, pl.ka, pl.stages);
   char* w = static_cast<char*>(ws);
   size_t off = 0;
   float* carry = reinterpret_cast<float*>(w);

@@ -690,6 +690,25 @@ cudaError_t launch_variant(int variant, const CArgs& a, const ClusterShape& cs, 
 
 }  // namespace
 
+bool cluster_kernel_attrs(int variant, bool backward, int* regs, int* local_bytes, int* max_threads) {
+  const void* f;
+  switch (variant) {
+    case kElman: f = backward ? (const void*)cl_bwd_kernel<kElman, 16> : (const void*)cl_fwd_kernel<kElman, 16>; break;
+    case kLstm: f = backward ? (const void*)cl_bwd_kernel<kLstm, 16> : (const void*)cl_fwd_kernel<kLstm, 16>; break;
+    case kGru: f = backward ? (const void*)cl_bwd_kernel<kGru, 16> : (const void*)cl_fwd_kernel<kGru, 16>; break;
+    default: f = backward ? (const void*)cl_bwd_kernel<kSlstm, 16> : (const void*)cl_fwd_kernel<kSlstm, 16>; break;
+  }
+  cudaFuncAttributes at{};
+  if (cudaFuncGetAttributes(&at, f) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  *regs = at.numRegs;
+  *local_bytes = (int)at.localSizeBytes;
+  *max_threads = at.maxThreadsPerBlock;
+  return true;
+}
+
 size_t cluster_forward_ws(const Problem& p, const Plan& pl) {
   return cluster_shape(p, pl.units_per_cta, pl.batch_tile, false).ws;
 }

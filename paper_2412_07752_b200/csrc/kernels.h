@@ -35,6 +35,7 @@ struct Plan {
   int groups;          // heads x batch tiles
   int grid, threads, smem_bytes, tmem_cols, k_split;
   int cluster;         // >0: cluster-resident fused kernels with this cluster size
+  int ka, stages;      // alternating path: K atoms per pipeline stage, ring depth
   size_t ws_bytes;
   double solve_us;
 };
@@ -66,6 +67,9 @@ cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStre
 cudaError_t cluster_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 size_t cluster_forward_ws(const Problem& p, const Plan& pl);
 size_t cluster_backward_ws(const Problem& p, const Plan& pl);
+// Registers per thread / local (spill) bytes of the cluster kernel the plan
+// would launch (compiler feedback for the planner); false without a device.
+bool cluster_kernel_attrs(int variant, bool backward, int* regs, int* local_bytes, int* max_threads);
 
 // ---- alternating path (alternating.cu) ----
 struct AltShape {
@@ -79,7 +83,9 @@ struct AltShape {
   uint32_t stage_bytes, a_bytes, region, tmem_cols;
   size_t smem;
 };
-AltShape alt_shape(const Problem& p, bool backward, int sm_count);
+AltShape alt_shape(const Problem& p, bool backward, int N, int KS, int ka, int stages);
+constexpr uint32_t kAltAStage = 128 * 64 * 2;  // A bytes per K atom (128 rows x 64 bf16)
+constexpr int kAltMaxKS = 8;
 bool alt_supported(const Problem& p, std::string* why);
 cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);

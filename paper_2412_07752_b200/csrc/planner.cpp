@@ -1,17 +1,31 @@
-// planner.cpp -- tiling solver for the B200 kernels.
+// planner.cpp -- the B200 tiling solver: integer CSPs in the ConstrINT style
+// (reference planner.cpp:100-313), solved by csp.cpp.
 //
-// First version: explicit enumeration over the (small) candidate domains with
-// the same constraints the CSP formulation uses (TMEM columns, SMEM bytes,
-// co-residency, tcgen05 shape rules).  Replaced by the propagating CSP solver
-// in csp.cpp.
+// The reference encodes an Ampere/Hopper fused kernel (13 E/W/B/L variables
+// per axis, register/SRAM footprints).  The B200 kernels have different
+// resources, so each kernel family gets its own formulation over B200 limits
+// queried from the device: SMEM opt-in bytes, TMEM columns (512 x 128 lanes x
+// 32 bit per SM), thread-block cluster size (16 non-portable), SM count
+// (co-residency), tcgen05 shapes (M = 128 TMEM block + M = 64 SMEM block,
+// N = 16-wide batch tiles, K = 16) and TMA box/stage sizes.  As in the
+// reference, a heuristic order + value preference picks among feasible
+// tilings (planner.cpp:203-228: minimise the synchronising / accumulating
+// blocks first), and the reference's missing compiler-feedback loop
+// is closed: the chosen kernel's register count and
+// spill bytes (cudaFuncGetAttributes) are checked and, if the launch would not
+// fit, a tighter thread constraint is added and the CSP re-solved.
 #include "planner.h"
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <optional>
 
 #include "../../include/flashrnn.h"
+#include "csp.h"
 
 namespace frnn {
 
@@ -33,9 +47,230 @@ const DeviceLimits& device_limits() {
   return lim;
 }
 
-static int ngp_of(int NG) { return NG <= 1 ? 1 : NG <= 2 ? 2 : 4; }
+namespace {
 
-static bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
+using csp::Domain;
+using csp::Int;
+using csp::Pref;
+using csp::Rel;
+
+int ngp_of(int NG) { return NG <= 1 ? 1 : NG <= 2 ? 2 : 4; }
+
+// Readable constraint building on top of csp::Problem (node handles).
+struct Builder {
+  csp::Problem p;
+  std::map<std::string, int> var_of;
+  struct E {
+    Builder* b;
+    int n;
+    E operator+(E o) const { return {b, b->p.add(n, o.n)}; }
+    E operator*(E o) const { return {b, b->p.mul(n, o.n)}; }
+    E operator+(Int c) const { return *this + b->k(c); }
+    E operator*(Int c) const { return *this * b->k(c); }
+  };
+  E var(const std::string& id, Domain d) {
+    const int v = p.add_var(id, std::move(d));
+    var_of[id] = v;
+    return {this, p.leaf(v)};
+  }
+  E k(Int c) { return {this, p.constant(c)}; }
+  void le(E a, E b) { p.require(Rel::Le, a.n, b.n); }
+  void le(E a, Int c) { le(a, k(c)); }
+  void le(Int c, E b) { le(k(c), b); }
+  void eq(E a, E b) { p.require(Rel::Eq, a.n, b.n); }
+  void eq(E a, Int c) { eq(a, k(c)); }
+  void divides(Int c, E b) { p.require(Rel::Div, k(c).n, b.n); }
+  void prefer(const std::string& id, Pref pr) { p.prefer(var_of.at(id), pr); }
+};
+
+// ---------------------------------------------------------------------------
+// Cluster-resident fused kernels (fused_cluster.cu).  Per group (head x batch
+// tile of 16 rows) one cluster of CL CTAs; CTA p owns UPC hidden units and all
+// NG gates of them: rows = NGP*UPC gate rows, R1 of them as the TMEM A operand
+// (M=128 block), R2 = rows - R1 in SMEM (M=64 block, allocated as 64 rows).
+// `thread_cap`: feedback bound on threads per CTA (0 = none).
+Builder cluster_csp(const Problem& p, int pass, const DeviceLimits& lim, int thread_cap) {
+  Builder b;
+  const int NGP = ngp_of(p.NG), N = 16, DH = p.DH;
+  const int MB = (DH + 127) / 128;
+  const int nbt_max = (p.B + N - 1) / N;
+  auto UPC = b.var("UPC", Domain::grid(8, std::max(8, std::min(DH, 128)), 8));
+  auto CL = b.var("CL", Domain::span(1, lim.cluster_max));
+  auto NB = b.var("NB", Domain::span(1, nbt_max));
+  auto R1 = b.var("R1", Domain::span(1, lim.umma_m));
+  auto R2P = b.var("R2P1", Domain::span(1, 65));        // R2 + 1
+  auto A2P = b.var("A2P1", Domain::set({1, 65}));        // SMEM block rows + 1 (0 or 64)
+  b.eq(UPC * CL, DH);                                    // every unit owned once
+  b.divides(16, b.k(DH));                                // 16-byte h chunks, K multiple of 16
+  b.le(p.B, NB * N);                                     // batch tiles cover B
+  b.eq(UPC * NGP + 1, R1 + R2P);                         // rows = R1 (TMEM) + R2 (SMEM)
+  b.le(R2P, A2P);                                        // SMEM block present iff R2 > 0
+  b.le(UPC * (N / 2), thread_cap > 0 ? std::min(384, thread_cap) : 384);  // one unit pair per thread
+  b.le(CL * NB * p.NH, lim.sm_count);                    // all clusters co-resident
+  if (pass == 0) {
+    // SMEM: double-buffered h tile [N x DH], SMEM A block, fp32 accumulator
+    // staging [N][rows+1], own h slice, barriers (fused_cluster.cu cluster_shape)
+    b.le(A2P * (DH * 2) + UPC * (N * NGP * 4 + N * 2) + (4 * N * DH + N * 4 + 64),
+         lim.smem_optin + DH * 2);
+    // TMEM: R slice as bf16 pairs (DH/2 columns, 32-aligned) + two N-wide accumulators
+    b.le(b.k(((DH / 2 + 31) / 32) * 32 + 2 * N), lim.tmem_cols);
+  } else {
+    // Backward: R_p^T as MB 128-column blocks (MBT in TMEM, the rest in SMEM),
+    // K = rows padded to 16 (KBH = K/2 TMEM columns per block)
+    auto MBT = b.var("MBT", Domain::span(1, MB));
+    auto KBH = b.var("KBH", Domain::grid(8, 128, 8));
+    b.le(UPC * NGP, KBH * 2);
+    b.le(KBH * 2, UPC * NGP + 15);
+    b.le(MBT * KBH + MB * N, lim.tmem_cols);
+    // SMEM: (MB-MBT) blocks [128 x K] + partial receive [CL][N][UPC] fp32 + dg tile + db scratch
+    b.le(KBH * (MB * 512 + N * 4) + CL * UPC * (N * 4) + UPC * (p.NG * N * 4) + 64,
+         b.k(lim.smem_optin) + MBT * KBH * 512);
+  }
+  // Heuristic (planner.cpp:203-228 in spirit): fewest CTAs synchronising per
+  // step, fewest batch tiles, fill TMEM before SMEM, most R^T in TMEM.
+  b.prefer("CL", Pref::Smallest);
+  b.prefer("NB", Pref::Smallest);
+  b.prefer("R1", Pref::Largest);
+  if (pass == 1) {
+    b.prefer("MBT", Pref::Largest);
+    b.prefer("KBH", Pref::Smallest);
+  }
+  b.prefer("A2P1", Pref::Smallest);
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// Alternating path (alternating.cu): per-step TMA-streamed GEMM.  Batch tile N
+// (MMA N) x NB tiles, K atoms per stage KA, ring depth ST, backward cluster
+// K-split KS; one wave of CTAs.
+Builder alt_csp(const Problem& p, int pass, const DeviceLimits& lim) {
+  Builder b;
+  const int DH = p.DH;
+  int nrec = 0;
+  for (int j = 0; j < p.NG; ++j) nrec += p.rec[j];
+  const int ring = getenv("FRNN_ALT_SMEM_KB") ? atoi(getenv("FRNN_ALT_SMEM_KB")) * 1024 : 200 * 1024;
+  auto N = b.var("N", Domain::grid(16, 128, 16));
+  auto NB = b.var("NB", Domain::span(1, (p.B + 15) / 16));
+  auto KA = b.var("KA", Domain::span(1, 2));
+  auto KPG = b.var("KPG", Domain::span(1, std::max(1, DH / 64)));
+  auto ST = b.var("ST", Domain::span(2, 8));
+  b.le(p.B, N * NB);
+  b.eq(KA * KPG * 64, DH);                                        // whole 64-wide K atoms
+  b.le(ST * KA * (int)kAltAStage + ST * KA * N * 128 + 2048, ring);  // stage ring
+  if (pass == 0) {
+    const int UPT = p.NG == 1 ? 128 : 32;
+    b.le(N * 512 + (512 + 2048), lim.smem_optin);                 // epilogue [128][N+1] fp32
+    b.le(NB * ((DH + UPT - 1) / UPT * p.NH), std::max(lim.sm_count, (DH + UPT - 1) / UPT * p.NH));
+    b.prefer("NB", Pref::Smallest);
+  } else {
+    auto KS = b.var("KS", Domain::span(1, kAltMaxKS));
+    b.le(KS, KPG * std::max(1, nrec));                            // every rank has K blocks
+    if (nrec == 0) b.eq(KS, 1);
+    b.le(N * 528 + 2048, lim.smem_optin);                         // epilogue [N][132] fp32
+    b.le(KS * NB * ((DH + 127) / 128 * p.NH), std::max(lim.sm_count, (DH + 127) / 128 * p.NH));
+    b.prefer("NB", Pref::Smallest);
+    b.prefer("KS", Pref::Largest);  // spread the per-step R^T stream over the SMs
+  }
+  b.prefer("N", Pref::Smallest);
+  b.prefer("KA", Pref::Largest);
+  b.prefer("ST", Pref::Largest);
+  return b;
+}
+
+std::optional<std::map<std::string, Int>> run(const Builder& b) {
+  const auto sol = csp::solve(b.p);
+  if (!sol) return std::nullopt;
+  return sol->values;
+}
+
+bool plan_cluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
+  if (getenv("FRNN_NO_CLUSTER")) {
+    *why = "cluster kernels disabled (FRNN_NO_CLUSTER)";
+    return false;
+  }
+  int cap = 0;
+  for (int round = 0; round < 3; ++round) {
+    const auto sol = run(cluster_csp(p, pass, lim, cap));
+    if (!sol) {
+      *why = "cluster: no tiling satisfies the B200 TMEM/SMEM/cluster constraints";
+      return false;
+    }
+    const int upc = (int)sol->at("UPC"), CL = (int)sol->at("CL");
+    const ClusterShape cs = cluster_shape(p, upc, 16, pass == 1);
+    if (!cluster_ept_supported(cs.EPT) || (pass == 1 && cs.MBT < 1)) {
+      *why = "cluster: solver/launcher geometry mismatch";
+      return false;
+    }
+    // Compiler feedback: the launch must fit the register file without spills.
+    int regs = 0, local = 0, maxt = 0;
+    if (cluster_kernel_attrs(p.variant, pass == 1, &regs, &local, &maxt) &&
+        ((long long)regs * cs.threads > lim.regs_per_sm || cs.threads > maxt)) {
+      cap = std::min(maxt, (int)(lim.regs_per_sm / std::max(1, regs))) / 128 * 128;
+      if (cap < 128) {
+        *why = "cluster: kernel register use leaves no feasible block size";
+        return false;
+      }
+      continue;
+    }
+    Plan& pl = *out;
+    pl = Plan{};
+    pl.algo = FRNN_ALGO_FUSED;
+    pl.cluster = CL;
+    pl.rows_per_cta = upc * ngp_of(p.NG);
+    pl.batch_tile = 16;
+    pl.units_per_cta = upc;
+    pl.ctas_per_group = CL;
+    pl.groups = cs.groups;
+    pl.grid = cs.groups * CL;
+    pl.threads = cs.threads;
+    pl.smem_bytes = (int)cs.smem;
+    pl.tmem_cols = (int)cs.tmem_cols;
+    pl.k_split = 1;
+    pl.ws_bytes = pass == 0 ? cluster_forward_ws(p, pl) : cluster_backward_ws(p, pl);
+    return true;
+  }
+  *why = "cluster: compiler feedback did not converge";
+  return false;
+}
+
+bool plan_alt(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
+  if (!alt_supported(p, why)) return false;
+  const auto sol = run(alt_csp(p, pass, lim));
+  if (!sol) {
+    *why = "alternating path: no tiling satisfies the B200 constraints";
+    return false;
+  }
+  const int N = (int)sol->at("N"), KA = (int)sol->at("KA"), ST = (int)sol->at("ST");
+  const int KS = pass == 1 ? (int)sol->at("KS") : 1;
+  const AltShape sh = alt_shape(p, pass == 1, N, KS, KA, ST);
+  if ((int)sh.smem > lim.smem_optin) {
+    *why = "alternating path: shared memory";
+    return false;
+  }
+  Plan& pl = *out;
+  pl = Plan{};
+  pl.algo = FRNN_ALGO_ALTERNATING;
+  pl.rows_per_cta = 128;
+  pl.batch_tile = N;
+  pl.units_per_cta = pass == 0 ? sh.UPT : 128 / KS;
+  pl.ctas_per_group = KS;
+  pl.groups = sh.tiles * p.NH * sh.NBT;
+  pl.grid = sh.grid;
+  pl.threads = 256;
+  pl.smem_bytes = (int)sh.smem;
+  pl.tmem_cols = (int)sh.tmem_cols;
+  pl.k_split = KS;
+  pl.cluster = KS > 1 ? KS : 0;
+  pl.ka = KA;
+  pl.stages = ST;
+  pl.ws_bytes = pass == 0 ? alt_forward_ws(p, pl) : alt_backward_ws(p, pl);
+  return true;
+}
+
+// L2-flag fused kernels (fused_bf16.cu): the measured baseline of the cluster
+// design, used when no cluster shape fits.  Largest units-per-CTA that divides
+// DH with the grid co-resident.
+bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
   const int NGP = ngp_of(p.NG);
   const int N = 16;
   if (p.DH % 8) {
@@ -54,7 +289,6 @@ static bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan
     *why = "fused: shared memory";
     return false;
   }
-  // Largest units-per-CTA that divides DH (fewest CTAs to synchronise).
   int best = 0;
   for (int upc = 128 / NGP; upc >= 1; --upc)
     if (p.DH % upc == 0) {
@@ -84,47 +318,7 @@ static bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan
   return true;
 }
 
-// Cluster-resident fused kernels (fused_cluster.cu): largest units-per-CTA
-// (fewest CTAs in the cluster) whose slice fits TMEM (<=128 rows) + one M=64
-// SMEM block, with cluster size <= 16 and SMEM/TMEM within the device limits.
-static bool plan_cluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
-  const int NGP = ngp_of(p.NG);
-  const int N = 16;
-  if (p.DH % 16 || p.DH > 960) {
-    *why = "cluster: head_dim must be a multiple of 16 and <= 960";
-    return false;
-  }
-  for (int upc : {48, 32, 16, 8}) {
-    if (p.DH % upc) continue;
-    const int rows = upc * NGP, CL = p.DH / upc;
-    if (rows > 192 || CL > 16) continue;
-    ClusterShape cf = cluster_shape(p, upc, N, false), cb = cluster_shape(p, upc, N, true);
-    if (!cluster_ept_supported(cf.EPT)) continue;
-    const ClusterShape& cs = pass == 0 ? cf : cb;
-    if ((int)cs.tmem_cols > lim.tmem_cols || (int)cs.smem > lim.smem_optin) continue;
-    if (pass == 1 && cb.MBT < 1) continue;
-    Plan& pl = *out;
-    pl = Plan{};
-    pl.algo = FRNN_ALGO_FUSED;
-    pl.cluster = CL;
-    pl.rows_per_cta = rows;
-    pl.batch_tile = N;
-    pl.units_per_cta = upc;
-    pl.ctas_per_group = CL;
-    pl.groups = cs.groups;
-    pl.grid = cs.groups * CL;
-    pl.threads = cs.threads;
-    pl.smem_bytes = (int)cs.smem;
-    pl.tmem_cols = (int)cs.tmem_cols;
-    pl.k_split = 1;
-    pl.ws_bytes = pass == 0 ? cluster_forward_ws(p, pl) : cluster_backward_ws(p, pl);
-    return true;
-  }
-  *why = "cluster: no units-per-CTA fits (cluster <= 16, rows <= 192)";
-  return false;
-}
-
-static bool plan_simt(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
+bool plan_simt(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
   const size_t smem = simt_smem_bytes(p, pass == 1);
   if ((int)smem > lim.smem_optin) {
     *why = "simt: R block does not fit in shared memory";
@@ -147,6 +341,13 @@ static bool plan_simt(const Problem& p, int pass, const DeviceLimits& lim, Plan*
   return true;
 }
 
+}  // namespace
+
+std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimits& lim) {
+  if (algo == FRNN_ALGO_ALTERNATING) return csp::format(alt_csp(p, pass, lim).p);
+  return csp::format(cluster_csp(p, pass, lim, 0).p);
+}
+
 int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Plan* out, std::string* why) {
   if (!p.bf16) {
     if (algo != FRNN_ALGO_AUTO && algo != FRNN_ALGO_SIMT) {
@@ -159,37 +360,18 @@ int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Pl
     *why = "bf16 mode has no SIMT path";
     return FRNN_EUNSUPPORTED;
   }
+  std::string w1, w2, w3;
   if (algo == FRNN_ALGO_AUTO || algo == FRNN_ALGO_FUSED) {
-    if (!getenv("FRNN_NO_CLUSTER") && plan_cluster(p, pass, lim, out, why)) return FRNN_OK;
-    if (plan_fused(p, pass, lim, out, why)) return FRNN_OK;
-    if (algo == FRNN_ALGO_FUSED) return FRNN_EINFEASIBLE;
+    if (plan_cluster(p, pass, lim, out, &w1)) return FRNN_OK;
+    if (plan_fused(p, pass, lim, out, &w2)) return FRNN_OK;
+    if (algo == FRNN_ALGO_FUSED) {
+      *why = w1 + "; " + w2;
+      return FRNN_EINFEASIBLE;
+    }
   }
-  std::string alt_why;
-  if (!alt_supported(p, &alt_why)) {
-    *why = why->empty() ? alt_why : *why + "; " + alt_why;
-    return FRNN_EINFEASIBLE;
-  }
-  const AltShape sh = alt_shape(p, pass == 1, lim.sm_count);
-  if ((int)sh.smem > lim.smem_optin) {
-    *why = "alternating path: shared memory";
-    return FRNN_EINFEASIBLE;
-  }
-  Plan& pl = *out;
-  pl = Plan{};
-  pl.algo = FRNN_ALGO_ALTERNATING;
-  pl.rows_per_cta = 128;
-  pl.batch_tile = sh.N;
-  pl.units_per_cta = pass == 0 ? sh.UPT : 128 / sh.KS;
-  pl.ctas_per_group = sh.KS;
-  pl.groups = sh.tiles * p.NH * sh.NBT;
-  pl.grid = sh.grid;
-  pl.threads = 256;
-  pl.smem_bytes = (int)sh.smem;
-  pl.tmem_cols = (int)sh.tmem_cols;
-  pl.k_split = sh.KS;
-  pl.cluster = sh.KS > 1 ? sh.KS : 0;
-  pl.ws_bytes = pass == 0 ? alt_forward_ws(p, pl) : alt_backward_ws(p, pl);
-  return FRNN_OK;
+  if (plan_alt(p, pass, lim, out, &w3)) return FRNN_OK;
+  *why = algo == FRNN_ALGO_AUTO ? w1 + "; " + w2 + "; " + w3 : w3;
+  return FRNN_EINFEASIBLE;
 }
 
 }  // namespace frnn

@@ -15,7 +15,7 @@ struct DeviceLimits {
   int regs_per_sm = 65536;        // 32-bit registers
   int tmem_cols = 512;            // TMEM columns (x 128 lanes x 32 bit) per SM
   int max_threads = 1024;
-  int cluster_max = 8;
+  int cluster_max = 16;            // non-portable thread-block cluster size
   int umma_m = 128;               // tcgen05 kind::f16 M with cta_group::1
   int umma_k = 16;                // tcgen05 kind::f16 K per instruction
 };
@@ -25,5 +25,9 @@ const DeviceLimits& device_limits();
 // Returns an frnn_status; *why explains infeasibility.
 int solve_plan(const Problem& p, int pass, int algo_request, const DeviceLimits& lim, Plan* out,
                std::string* why);
+
+// The tiling CSP of a kernel family (FRNN_ALGO_FUSED: cluster-resident kernels,
+// FRNN_ALGO_ALTERNATING) in the text form of include/flashrnn_csp.h.
+std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimits& lim);
 
 }  // namespace frnn

@@ -177,3 +177,37 @@ def test_divisibility_and_progression_domains():
     # a*a == b with no a | ... : infeasible when b is prime
     assert csp_solve("v a R r 1 50\nv b C r 97 97\nn v 0\nn v 1\nn * 0 0\nc = 2 1\n")[0] is None
     assert csp_solve("v a R r 1 50\nv b C r 49 49\nn v 0\nn v 1\nn * 0 0\nc = 2 1\n")[0] == {"a": 7}
+
+
+# ------------------------------------ the B200 planner's own tiling CSPs ----
+def plan_csp(variant, B, NH, DH, pas, algo):
+    from paper_2412_07752_b200.abi import Shape, cell_spec, load
+    L = load()
+    L.frnn_debug_plan_csp.argtypes = [C.c_void_p, Shape, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_size_t]
+    buf = C.create_string_buffer(1 << 20)
+    cell = cell_spec(variant)
+    assert L.frnn_debug_plan_csp(C.byref(cell), Shape(1024, B, NH, DH), 1, pas, algo, buf, len(buf)) == 0
+    return buf.value.decode()
+
+
+@pytest.mark.parametrize("variant,B,NH,DH,pas,algo", [
+    ("slstm", 16, 1, 768, 0, 1), ("slstm", 16, 1, 768, 1, 1),   # config 2, cluster-resident kernels
+    ("lstm", 16, 12, 64, 1, 1), ("lstm", 16, 4, 192, 0, 1),     # config 3
+    ("gru", 16, 1, 768, 1, 1),                                  # config 4
+    ("slstm", 64, 1, 3072, 0, 2), ("slstm", 64, 1, 3072, 1, 2),  # config 5, alternating path
+])
+def test_b200_planner_csp_matches_reference_solver(ref, variant, B, NH, DH, pas, algo):
+    """The B200 formulation (planner.cpp) solved by the reference ConstrINT
+    solver gives the tiling the planner chose."""
+    from paper_2412_07752_b200.abi import plan as frnn_plan
+    text = plan_csp(variant, B, NH, DH, pas, algo)
+    mine, st = csp_solve(text)
+    assert mine is not None
+    assert ref_solve(ref, text) == mine
+    plan = frnn_plan(variant, 1024, B, NH, DH, "bf16", ["forward", "backward"][pas])
+    if algo == 1:
+        ngp = 1 if variant == "elman" else 4
+        assert (plan["ctas_per_group"], plan["rows_per_cta"]) == (mine["CL"], mine["UPC"] * ngp)
+    else:
+        assert plan["batch_tile"] == mine["N"] and plan["k_split"] == mine.get("KS", 1)
+    print(variant, DH, pas, mine, f"{st['solve_us']:.0f} us")
