@@ -29,6 +29,8 @@
 // MMAs are issued by warp 0 as whole-warp PTX loops (sm100.cuh mma_chain_*).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "cells.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
@@ -60,6 +62,7 @@ struct CArgs {
   float* dbacc;    // [NBT][NG][D]
   long long* prof;
   int prof_steps;
+  int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
 };
 
 #define FRNN_PROF(slot, step)                                              \
@@ -159,13 +162,17 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   const size_t xo = (size_t)(b0 + b) * NG * D + e;  // offset in [.][B][NG][D] tensors
   const size_t sstep = (size_t)NS * B * D, gstep = (size_t)NG * B * D;
   float st[NS][2], bj[NG][2];
-  uint32_t xr[NG];
+  uint32_t xr[NG], xn[NG];
+  float gsave[NG][2], nsave[NS][2];  // step t-1 outputs, stored while MMA(t) runs
 #pragma unroll
   for (int j = 0; j < NG; ++j) {
     bj[j][0] = own ? bf(bias, (size_t)j * D + e) : 0.f;
     bj[j][1] = own ? bf(bias, (size_t)j * D + e + 1) : 0.f;
-    xr[j] = 0;
+    xr[j] = xn[j] = 0;
+    gsave[j][0] = gsave[j][1] = 0.f;
   }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) nsave[s][0] = nsave[s][1] = 0.f;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     const uint32_t v = valid ? ld2(s0, (size_t)s * B * D + so) : 0u;
@@ -207,6 +214,24 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         mma_chain_ts(tbase + a.acc1, tbase, 8, bd, (2 * LBO) >> 4, idesc1, K / 16);
       if (elect_one()) mma_commit(&bars[0]);
       __syncwarp();
+    }
+    // Off the critical path, while MMA(t) runs: the trace of step t-1 and the
+    // x_{t+1} prefetch (predicated loads: issuing never waits for them).
+    if (valid) {
+      if (t > 0) {
+        bf16* gdst = gates + (size_t)(t - 1) * gstep + so;
+        bf16* sdst = states + (size_t)t * sstep + so;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) st2(gdst, (size_t)j * B * D, gsave[j][0], gsave[j][1]);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) st2(sdst, (size_t)s * B * D, nsave[s][0], nsave[s][1]);
+      }
+      if (t + 1 < T) {
+        const bf16* xp = x + (size_t)(t + 1) * gstep + xo;
+#pragma unroll
+        for (int j = 0; j < NG; ++j)
+          if (p.inp[j]) xn[j] = ld2(xp, (size_t)j * D);
+      }
     }
     mbar_wait(&bars[0], t & 1);
     tc_fence_after();
@@ -263,21 +288,25 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       }
     }
     FRNN_PROF(4, t);
-    // Off the critical path: the trace, and x_{t+1} (bf16x2 accesses).
-    if (valid) {
-      bf16* gdst = gates + (size_t)t * gstep + so;
-      bf16* sdst = states + (size_t)(t + 1) * sstep + so;
 #pragma unroll
-      for (int j = 0; j < NG; ++j) st2(gdst, (size_t)j * B * D, gout[j][0], gout[j][1]);
-#pragma unroll
-      for (int s = 0; s < NS; ++s) st2(sdst, (size_t)s * B * D, nout[s][0], nout[s][1]);
-      if (t + 1 < T) {
-        const bf16* xn = x + (size_t)(t + 1) * gstep + xo;
-#pragma unroll
-        for (int j = 0; j < NG; ++j)
-          if (p.inp[j]) xr[j] = ld2(xn, (size_t)j * D);
-      }
+    for (int j = 0; j < NG; ++j) {
+      gsave[j][0] = gout[j][0];
+      gsave[j][1] = gout[j][1];
+      xr[j] = xn[j];
     }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      nsave[s][0] = nout[s][0];
+      nsave[s][1] = nout[s][1];
+    }
+  }
+  if (valid && T > 0) {  // the last step's trace
+    bf16* gdst = gates + (size_t)(T - 1) * gstep + so;
+    bf16* sdst = states + (size_t)T * sstep + so;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) st2(gdst, (size_t)j * B * D, gsave[j][0], gsave[j][1]);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) st2(sdst, (size_t)s * B * D, nsave[s][0], nsave[s][1]);
   }
   tc_fence_before();
   __syncthreads();
@@ -312,19 +341,25 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const size_t blk_bytes = (size_t)128 * KBP * 2;
 
   extern __shared__ __align__(1024) uint8_t smem[];
+  const bool dsm = a.dsm != 0;
+  const int TP = a.UPC + 2;                                              // term pitch (bank spread)
   uint8_t* AS = smem;                                                    // (MB-MBT) x [128 x KBP] K-major
-  float* recv = reinterpret_cast<float*>(AS + (MB - MBT) * blk_bytes);  // [CL src][N][UPC]
-  uint8_t* dgB = reinterpret_cast<uint8_t*>(recv) + recv_bytes;         // [N x KBP] K-major
+  float* recv = reinterpret_cast<float*>(AS + (MB - MBT) * blk_bytes);  // global mode: [CL src][N][UPC]
+  float* recv1 = dsm ? recv + recv_bytes / 4 : recv;                    // DSMEM mode: 2 x [CL src][UPC][N]
+  uint8_t* dgB = reinterpret_cast<uint8_t*>(recv1) + recv_bytes;        // [N x KBP] K-major
   float* dbs = reinterpret_cast<float*>(dgB + N * KBP * 2);             // [NG][N][UPC] db scratch
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dbs + NG * N * a.UPC);   // mma, rcv, rdy0, rdy1
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bars + 4);
+  float* term = dbs + NG * N * a.UPC;                                    // DSMEM mode: [N][TP] summed R^T dg
+  uint64_t* bars = reinterpret_cast<uint64_t*>(term + (dsm ? N * TP : 0));  // -, rcv, rdy0|rcv0, rdy1|rcv1
+  uint64_t* blkbar = bars + 4;  // [MB]: MMA of column block mb (and all before it) complete
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(blkbar + 8);
 
   if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], a.CL);
-    mbar_init(&bars[3], a.CL);
+    mbar_init(&bars[2], dsm ? 1 : a.CL);
+    mbar_init(&bars[3], dsm ? 1 : a.CL);
+    for (int i = 0; i < MB; ++i) mbar_init(&blkbar[i], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < N * KBP * 2 / 16; i += NT) reinterpret_cast<uint4*>(dgB)[i] = make_uint4(0, 0, 0, 0);
@@ -405,8 +440,45 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
 
   // Partials of step s are in pstage[grp][s&1][me][*]: wait for the CL
   // producers, pull them with one bulk load, sum, clip, add to ds_h.
-  uint32_t rcv_phase = 0;
+  uint32_t rcv_phase = 0, par_phase = 0;
+  auto absorb_dsm = [&](int s) {  // partials pushed into my recv[s&1] by every peer (st.async)
+    const int pb = s & 1;
+    if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
+    mbar_wait_cluster(&bars[2 + pb], (par_phase >> pb) & 1u);
+    par_phase ^= 1u << pb;
+    const float* rb = pb ? recv1 : recv;  // [src][cu][N]
+    if (tid < a.UPC * (N / 4)) {          // sum over sources: one float4 of 4 batch rows per thread
+      const int cu = tid / (N / 4), g = tid % (N / 4);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
+        const float4 v = *reinterpret_cast<const float4*>(rb + ((size_t)q * a.UPC + cu) * N + 4 * g);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      term[(4 * g + 0) * TP + cu] = acc.x;
+      term[(4 * g + 1) * TP + cu] = acc.y;
+      term[(4 * g + 2) * TP + cu] = acc.z;
+      term[(4 * g + 3) * TP + cu] = acc.w;
+    }
+    __syncthreads();
+    if (own) {
+      const float2 v = *reinterpret_cast<const float2*>(term + b * TP + u);
+      float t0 = v.x, t1 = v.y;
+      if (p.clip_mode == 1) {
+        t0 = fminf(fmaxf(t0, -mag), mag);
+        t1 = fminf(fmaxf(t1, -mag), mag);
+      }
+      ds[0][0] += t0;
+      ds[0][1] += t1;
+    }
+  };
   auto absorb = [&](int s) {
+    if (dsm) {
+      absorb_dsm(s);
+      return;
+    }
     const int pb = s & 1;
     const int kpub = T - 1 - s;  // publish order of step s
     if (w == 0) {
@@ -484,42 +556,53 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       fence_proxy_async_smem();
       __syncthreads();
       FRNN_PROF(2, k);
-      if (w == 0) {  // TMEM-A blocks then SMEM-A blocks, whole-warp PTX chains
+      if (w == 0) {  // column blocks in order (TMEM-A, then SMEM-A), one commit per block so
+                     // the drain + exchange of block mb overlaps the MMAs of the later blocks
         tc_fence_after();
         const uint64_t bd = sdesc_kmajor(smem_u32(dgB), LBO, SBO);
         const uint64_t ad = sdesc_kmajor(smem_u32(AS), 128 * 16, 128);
         const int nk = KBP / 16, cb = KBP / 2;
-        for (int mb = 0; mb < MBT; ++mb)
-          mma_chain_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
-        for (int mb = MBT; mb < MB; ++mb)
-          mma_chain_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)), (2 * 128 * 16) >> 4,
-                       bd, (2 * LBO) >> 4, idesc, nk);
-        if (elect_one()) mma_commit(&bars[0]);
-        __syncwarp();
+        for (int mb = 0; mb < MB; ++mb) {
+          if (mb < MBT)
+            mma_chain_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
+          else
+            mma_chain_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)),
+                         (2 * 128 * 16) >> 4, bd, (2 * LBO) >> 4, idesc, nk);
+          if (elect_one()) mma_commit(&blkbar[mb]);
+          __syncwarp();
+        }
       }
-      mbar_wait(&bars[0], mma_phase);
-      mma_phase ^= 1;
-      tc_fence_after();
       FRNN_PROF(3, k);
       // partial R_p^T dg_p, column c -> owner CTA c / UPC, layout [dest][src][b][u];
       // every warp drains the TMEM lane quadrant w%4 of blocks w/4, w/4+NT/128, ...
       float* base = a.pstage + (((size_t)grp * 2 + (t & 1)) * a.CL) * a.CL * N * a.UPC;
       const int qd = w & 3;
+      const uint32_t rb = smem_u32((t & 1) ? recv1 : recv), rbar = smem_u32(&bars[2 + (t & 1)]);
       for (int mb = w >> 2; mb < MB; mb += NT >> 7) {
+        mbar_wait(&blkbar[mb], mma_phase);
+        tc_fence_after();
         const int c = mb * 128 + 32 * qd + l;
         float v[16];
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + mb * N, v);
         if (c < DH) {
           const int q = c / a.UPC, cu = c % a.UPC;
-          float* dst = base + (((size_t)q * a.CL + me) * N) * a.UPC + cu;
+          if (dsm) {  // push straight into the owner's recv[t&1][me][cu][:], completing bytes on its mbarrier
+            const uint32_t dst = mapa_shared(rb + (uint32_t)(((me * a.UPC + cu) * N) * 4), q);
+            const uint32_t mbr = mapa_shared(rbar, q);
 #pragma unroll
-          for (int n = 0; n < N; ++n) dst[(size_t)n * a.UPC] = v[n];
+            for (int i = 0; i < N / 4; ++i) st_async_v4(dst + 16 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3], mbr);
+          } else {
+            float* dst = base + (((size_t)q * a.CL + me) * N) * a.UPC + cu;
+#pragma unroll
+            for (int n = 0; n < N; ++n) dst[(size_t)n * a.UPC] = v[n];
+          }
         }
       }
-      fence_proxy_async_global();
+      mma_phase ^= 1;
+      if (!dsm) fence_proxy_async_global();
       tc_fence_before();
       __syncthreads();
-      if (tid < a.CL) mbar_arrive_remote(mapa_shared(smem_u32(&bars[2 + (t & 1)]), tid));
+      if (!dsm && tid < a.CL) mbar_arrive_remote(mapa_shared(smem_u32(&bars[2 + (t & 1)]), tid));
       FRNN_PROF(4, k);
     }
     // Off the critical path: dx (= dg for input-wired gates, engine.hpp:311-316).
@@ -603,7 +686,12 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
     s.acc1 = (uint32_t)(s.MBT * colblk);
     s.tmem_cols = pow2_cols(s.acc1 + s.MB * N);
     s.smem = (size_t)(s.MB - s.MBT) * 128 * s.KBP * 2 + (size_t)s.CL * N * UPC * 4 + (size_t)N * s.KBP * 2 +
-             (size_t)p.NG * N * UPC * 4 + 64;
+             (size_t)p.NG * N * UPC * 4 + 128;  // + 4 exchange and 8 block mbarriers, TMEM base
+    // DSMEM exchange: a second (parity) receive buffer + the summed-term tile
+    const size_t dsm_smem = s.smem + (size_t)s.CL * N * UPC * 4 + (size_t)N * (UPC + 2) * 4;
+    const char* xe = getenv("FRNN_XCHG");  // A/B hook: 0 = global + TMA bulk load
+    s.dsm = (!xe || atoi(xe) != 0) && dsm_smem <= (size_t)kSmemOptin && (UPC % 4) == 0;
+    if (s.dsm) s.smem = dsm_smem;
     s.ws = align_up((size_t)s.groups * 2 * s.CL * s.CL * N * UPC * 4, 256);
   }
   return s;
@@ -633,6 +721,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.slice = cs.slice;
   a.prof = g_prof_buf;
   a.prof_steps = g_prof_steps;
+  a.dsm = backward && cs.dsm;
   char* w = static_cast<char*>(ws);
   if (!backward) {
     a.xstage = reinterpret_cast<bf16*>(w);

@@ -56,8 +56,10 @@ uint32_t fused_tmem_cols(const Problem& p, int N, bool backward);
 size_t fused_backward_ws(const Problem& p, const Plan& pl);
 
 // ---- cluster-resident fused path (fused_cluster.cu) ----
+constexpr int kSmemOptin = 232448;  // B200 max dynamic shared memory per CTA (opt-in)
 struct ClusterShape {
   int UPC, CL, R1, R2, K, KBP, MB, MBT, EPT, groups, threads;
+  bool dsm;  // backward: DSMEM partial exchange (else global + TMA bulk load)
   uint32_t acc1, acc2, tmem_cols, slice;
   size_t smem, ws;
 };

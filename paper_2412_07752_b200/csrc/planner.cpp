@@ -123,7 +123,7 @@ Builder cluster_csp(const Problem& p, int pass, const DeviceLimits& lim, int thr
     b.le(KBH * 2, UPC * NGP + 15);
     b.le(MBT * KBH + MB * N, lim.tmem_cols);
     // SMEM: (MB-MBT) blocks [128 x K] + partial receive [CL][N][UPC] fp32 + dg tile + db scratch
-    b.le(KBH * (MB * 512 + N * 4) + CL * UPC * (N * 4) + UPC * (p.NG * N * 4) + 64,
+    b.le(KBH * (MB * 512 + N * 4) + CL * UPC * (N * 4) + UPC * (p.NG * N * 4) + 128,
          b.k(lim.smem_optin) + MBT * KBH * 512);
   }
   // Heuristic (planner.cpp:203-228 in spirit): fewest CTAs synchronising per

@@ -160,6 +160,43 @@ __device__ __forceinline__ void mma_chain_ts_ss(uint32_t d1, uint32_t a1, uint32
       : "memory");
 }
 
+// K-outer / block-inner issue over several independent accumulators, so that
+// consecutive MMAs never target the same D (no accumulate-dependency stalls):
+//   for k < nk:  for i < nts: D[d0 + i*dstep] (+)= A_tmem[ta0 + i*tblk + 8k] . B(k)
+//                for i < nss: D[d0 + (nts+i)*dstep] (+)= A_smem[sa0 + i*sblk + k*sk] . B(k)
+// with B(k) = bd0 + k*bk and accumulate = (k > 0).  Whole warp; elect.sync issues.
+__device__ __forceinline__ void mma_kloop_multi(uint32_t d0, uint32_t dstep, uint32_t ta0, uint32_t tblk, int nts,
+                                                uint64_t sa0, uint64_t sblk, uint64_t sk, int nss, uint64_t bd0,
+                                                uint64_t bk, uint32_t idesc, int nk) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, q;\n\t.reg .b32 k, i, d, ta, tk;\n\t.reg .b64 bd, sa, sak;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 k, 0;\n\tmov.b64 bd, %9;\n\tmov.b32 tk, %2;\n\tmov.b64 sak, %5;\n\t"
+      "setp.ge.s32 q, k, %12;\n\t@q bra.uni MK_END%=;\n\t"
+      "MK_K%=:\n\t"
+      "setp.ne.b32 p, k, 0;\n\t"
+      "mov.b32 d, %0;\n\tmov.b32 ta, tk;\n\tmov.b32 i, 0;\n\t"
+      "setp.ge.s32 q, i, %4;\n\t@q bra.uni MK_TSE%=;\n\t"
+      "MK_TS%=:\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d], [ta], bd, %11, p;\n\t"
+      "add.u32 d, d, %1;\n\tadd.u32 ta, ta, %3;\n\tadd.s32 i, i, 1;\n\t"
+      "setp.lt.s32 q, i, %4;\n\t@q bra.uni MK_TS%=;\n\t"
+      "MK_TSE%=:\n\t"
+      "mov.b64 sa, sak;\n\tmov.b32 i, 0;\n\t"
+      "setp.ge.s32 q, i, %8;\n\t@q bra.uni MK_SSE%=;\n\t"
+      "MK_SS%=:\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d], sa, bd, %11, p;\n\t"
+      "add.u32 d, d, %1;\n\tadd.u64 sa, sa, %6;\n\tadd.s32 i, i, 1;\n\t"
+      "setp.lt.s32 q, i, %8;\n\t@q bra.uni MK_SS%=;\n\t"
+      "MK_SSE%=:\n\t"
+      "add.u32 tk, tk, 8;\n\tadd.u64 sak, sak, %7;\n\tadd.u64 bd, bd, %10;\n\tadd.s32 k, k, 1;\n\t"
+      "setp.lt.s32 q, k, %12;\n\t@q bra.uni MK_K%=;\n\t"
+      "MK_END%=:\n\t}" ::"r"(d0),
+      "r"(dstep), "r"(ta0), "r"(tblk), "r"(nts), "l"(sa0), "l"(sblk), "l"(sk), "r"(nss), "l"(bd0), "l"(bk),
+      "r"(idesc), "r"(nk)
+      : "memory");
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05.mma complete.
 __device__ __forceinline__ void mma_commit(uint64_t* mbar) {
   asm volatile(
@@ -383,6 +420,14 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 }
 // Wait until the preceding grid has completed and its writes are visible.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// 16-byte push into another CTA's shared memory (shared::cluster address),
+// completing 16 bytes on that CTA's mbarrier (shared::cluster address).
+__device__ __forceinline__ void st_async_v4(uint32_t dst, float a, float b, float c, float d, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+               : "memory");
+}
 
 // DSMEM load of a float from CTA `rank` at the same smem offset.
 __device__ __forceinline__ float ld_dsmem_f32(const void* local, uint32_t rank) {
