@@ -222,6 +222,28 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+// Blocking probe: the thread may be suspended (up to `ns`) until the phase
+// completes instead of re-polling -- waiting warps stop competing for issue
+// slots with the warps doing the step's work.
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t a, uint32_t phase, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_cluster_sleep(uint32_t a, uint32_t phase, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.b32 %0, "
+      "1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ bool mbar_try_cluster(uint32_t a, uint32_t phase) {
   uint32_t ok;
   asm volatile(
@@ -238,7 +260,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try(a, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try(a, phase))
+  while (!mbar_try_sleep(a, phase, 1000000u))
     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -332,7 +354,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
   const uint32_t a = smem_u32(bar);
   if (mbar_try_cluster(a, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_cluster(a, phase))
+  while (!mbar_try_cluster_sleep(a, phase, 1000000u))
     if (globaltimer_ns() - t0 > 4000000000ull) __trap();
 }
 // Arrive (count 1) on the mbarrier at cluster-shared address `remote`.
@@ -426,6 +448,13 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void st_async_v4(uint32_t dst, float a, float b, float c, float d, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
                "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_async_v4_b32(uint32_t dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                                uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(mbar)
                : "memory");
 }
 
