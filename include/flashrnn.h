@@ -151,6 +151,16 @@ FRNN_API int frnn_backward(const frnn_cell* cell, frnn_shape shape, int32_t dtyp
                   void* workspace, size_t workspace_bytes,
                   const frnn_options* opts, void* stream);
 
+/* -- the step before the path: input projection ---------------------------- */
+/* x = u . W^T, the gate pre-inputs rnnkit's engine takes already projected
+ * (SPEC.md:376):
+ *   u [tokens][in_features]            tokens = T*B, row-major (u[t][b][k])
+ *   W [out_features][in_features]      out_features = NG*D, row j*D + e
+ *   x [tokens][out_features]           = rnnkit's x[T][B][NG][D]
+ * bf16 in, fp32 accumulate (tcgen05), bf16 out; in_features % 8 == 0. */
+FRNN_API int frnn_input_projection(const void* W, const void* u, void* x, int64_t tokens, int32_t out_features,
+                                   int32_t in_features, int32_t dtype, void* stream);
+
 /* -- multi-GPU partitioner (batch x head sharding) --------------- */
 typedef struct {
   int32_t batch_begin, batch_end;   /* [begin, end) rows of B owned by this rank */

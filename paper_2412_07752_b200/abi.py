@@ -65,7 +65,8 @@ class Shard(C.Structure):
 
 
 EXPORTS = ["frnn_version", "frnn_last_error", "frnn_cell_spec", "frnn_plan", "frnn_workspace_size",
-           "frnn_forward", "frnn_backward", "frnn_partition", "frnn_csp_solve", "frnn_csp_brute_force"]
+           "frnn_forward", "frnn_backward", "frnn_partition", "frnn_csp_solve", "frnn_csp_brute_force",
+           "frnn_input_projection"]
 
 
 def lib_path() -> str:
@@ -188,6 +189,21 @@ class FlashRNN:
                                      x.data_ptr(), s0.data_ptr(), states.data_ptr(),
                                      gates.data_ptr(), ws.data_ptr(), ws.numel(), C.byref(o), s))
         return states, gates
+
+    def input_projection(self, W, u, x=None, stream=None):
+        """frnn_input_projection: x[T][B][NG*D] = u[T][B][Din] . W^T (W [NG*D][Din]), bf16."""
+        torch = self.torch
+        Din = u.shape[-1]
+        tokens = u.numel() // Din
+        out_f = W.shape[0]
+        if x is None:
+            x = torch.empty(tuple(u.shape[:-1]) + (out_f,), dtype=u.dtype, device=u.device)
+        s = stream if stream is not None else torch.cuda.current_stream(u.device).cuda_stream
+        self.lib.frnn_input_projection.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                                   C.c_int32, C.c_int32, C.c_void_p]
+        _check(self.lib.frnn_input_projection(W.data_ptr(), u.data_ptr(), x.data_ptr(), tokens, out_f, Din,
+                                              self._dtype(u), s))
+        return x
 
     def backward(self, variant, R, bias, states, gates, d_states_final, d_hidden=None, clip="off",
                  clip_mag=0.0, out=None, stream=None, algo="auto"):

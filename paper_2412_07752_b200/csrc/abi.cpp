@@ -289,6 +289,21 @@ int frnn_backward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const 
   return FRNN_OK;
 }
 
+int frnn_input_projection(const void* W, const void* u, void* x, int64_t tokens, int32_t out_features,
+                          int32_t in_features, int32_t dtype, void* stream) {
+  g_err.clear();
+  if (!W || !u || !x) return fail(FRNN_EINVAL_ARG, "null tensor pointer");
+  if (tokens < 1 || out_features < 1 || in_features < 1) return fail(FRNN_EINVAL_SHAPE, "degenerate shape");
+  if (dtype != FRNN_BF16) return fail(FRNN_EUNSUPPORTED, "input projection: bf16 only");
+  if (in_features % 8) return fail(FRNN_EINVAL_SHAPE, "in_features must be a multiple of 8 (16-byte TMA rows)");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaError_t e = frnn::wx_gemm(W, u, x, tokens, out_features, in_features, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return fail(FRNN_EUNSUPPORTED, "TMA tensor maps unavailable");
+  if (e != cudaSuccess) return cuda_fail(e, "input projection");
+  return FRNN_OK;
+}
+
 // Batch x head sharding over world_size ranks: heads split by the
 // largest factor of world_size dividing NH; the rest of world_size splits B.
 int frnn_partition(frnn_shape shape, int32_t world_size, int32_t rank, frnn_shard* out) {

@@ -109,6 +109,9 @@ cudaError_t dr_gemm(const Problem& p, const void* dg_dx_layout, cudaStream_t s);
 // db[i] = sum over batch tiles (fixed order) of acc[tile * n + i]
 cudaError_t db_convert(const float* acc, void* db, int n, int tiles, cudaStream_t s);
 
+// ---- input projection x = u W^T (wx_gemm.cu) ----
+cudaError_t wx_gemm(const void* W, const void* u, void* x, long long M, int N, int K, cudaStream_t s);
+
 // ---- utilities (util.cu) ----
 // Sets *flag (device int) to 1 if any of the n elements is non-finite.
 cudaError_t check_finite(const void* ptr, size_t n, bool bf16, int* flag, cudaStream_t s);
