@@ -14,6 +14,7 @@
 #include "rnnkit/rnn/engine.hpp"
 #include "rnnkit/rnn/gradcheck.hpp"
 #include "rnnkit/rnn/random_init.hpp"
+#include "rnnkit/rnn/tensor_io.hpp"
 
 using namespace rnnkit::rnn;
 
@@ -145,6 +146,47 @@ void ref_gradient_check(int v, int T, int DH, int NH, int B, uint64_t seed, doub
   GradCheckReport r = gradient_check(cfg);
   out4[0] = r.max_rel_inputs; out4[1] = r.max_rel_bias;
   out4[2] = r.max_rel_recurrent; out4[3] = r.max_rel_init_states;
+}
+
+// A complete reference case as an RTN1 file written by the reference's own
+// save_tensors (tensor_io.cpp:28-47): generator inputs (seeded as
+// ref_generate), the f64 forward trace and the f64 backward (clip off).
+int ref_save_case(const char* path, int v, int T, int B, int NH, int DH, uint64_t seed) {
+  try {
+    CellSpec c = spec(v);
+    Rng rng(seed * 7919 + 13);
+    Params<double> p = random_params(c, NH, DH, rng);
+    SequenceBatch<double> sb = random_batch(c, T, B, NH, DH, rng);
+    std::vector<double> dsf((size_t)c.num_states * B * NH * DH);
+    for (auto& d : dsf) d = rng.normal();
+    ForwardTrace<double> tr = forward(c, p, sb);
+    Gradients<double> g = backward(c, p, sb, tr, dsf);
+    const uint64_t D = (uint64_t)NH * DH, NS = c.num_states, NG = c.num_gates;
+    TensorMap t = params_to_tensors(p);
+    t["inputs"] = NamedTensor{{(uint64_t)T, (uint64_t)B, NG, D}, sb.inputs};
+    t["init_states"] = NamedTensor{{NS, (uint64_t)B, D}, sb.init_states};
+    t["d_states_final"] = NamedTensor{{NS, (uint64_t)B, D}, dsf};
+    t["states"] = NamedTensor{{(uint64_t)T + 1, NS, (uint64_t)B, D}, tr.states};
+    t["gates"] = NamedTensor{{(uint64_t)T, NG, (uint64_t)B, D}, tr.gates};
+    t["d_inputs"] = NamedTensor{{(uint64_t)T, (uint64_t)B, NG, D}, g.d_inputs};
+    t["d_bias"] = NamedTensor{{NG, D}, g.d_bias};
+    t["d_recurrent"] = NamedTensor{{(uint64_t)NH, NG, (uint64_t)DH, (uint64_t)DH}, g.d_recurrent};
+    t["d_init_states"] = NamedTensor{{NS, (uint64_t)B, D}, g.d_init_states};
+    save_tensors(path, t);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// Round trip through the reference reader + writer (load_tensors, save_tensors).
+int ref_rewrite_tensors(const char* in, const char* out) {
+  try {
+    save_tensors(out, load_tensors(in));
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 }  // extern "C"
