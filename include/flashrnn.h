@@ -132,6 +132,10 @@ FRNN_API int frnn_plan(const frnn_cell* cell, frnn_shape shape, int32_t dtype, i
               const frnn_options* opts, frnn_plan_info* out);
 FRNN_API int frnn_workspace_size(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
                         const frnn_options* opts, size_t* bytes);
+/* The plan as JSON (schema_version 1, the counterpart of rnnkit::plan::plan_to_json,
+ * planner.cpp:428-453): shape, kernel family, tiling, footprint, solve time. */
+FRNN_API int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                            const frnn_options* opts, char* out, size_t out_bytes);
 
 /* -- the hot path --------------------------------------------------------- */
 /* engine.hpp:143-203.  Writes states (incl. states[0] = s0) and gates. */

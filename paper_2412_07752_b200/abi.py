@@ -66,7 +66,7 @@ class Shard(C.Structure):
 
 EXPORTS = ["frnn_version", "frnn_last_error", "frnn_cell_spec", "frnn_plan", "frnn_workspace_size",
            "frnn_forward", "frnn_backward", "frnn_partition", "frnn_csp_solve", "frnn_csp_brute_force",
-           "frnn_input_projection"]
+           "frnn_input_projection", "frnn_plan_json"]
 
 
 def lib_path() -> str:
@@ -242,6 +242,19 @@ def plan(variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto") -> d
     _check(load().frnn_plan(C.byref(cell_spec(variant)), Shape(T, B, NH, DH), DTYPE[dtype], PASS[pass_],
                             C.byref(o), C.byref(info)))
     return info.as_dict()
+
+
+def plan_json(variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto") -> dict:
+    """frnn_plan_json (schema_version 1) parsed."""
+    import json
+    L = load()
+    L.frnn_plan_json.argtypes = [C.POINTER(Cell), Shape, C.c_int32, C.c_int32, C.POINTER(Options), C.c_char_p,
+                                 C.c_size_t]
+    buf = C.create_string_buffer(4096)
+    o = Options(0, ALGO[algo])
+    _check(L.frnn_plan_json(C.byref(cell_spec(variant)), Shape(T, B, NH, DH), DTYPE[dtype], PASS[pass_], C.byref(o),
+                            buf, len(buf)))
+    return json.loads(buf.value.decode())
 
 
 def csp_solve(problem: str) -> tuple[dict | None, dict]:

@@ -6,6 +6,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -179,6 +180,38 @@ int frnn_plan(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pa
   out->cluster = pl.cluster;
   out->workspace_bytes = (int64_t)pl.ws_bytes;
   out->solve_us = pl.solve_us;
+  return FRNN_OK;
+}
+
+// planner.cpp:428-453 plan_to_json, for the B200 plan (schema_version 1).
+int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass, const frnn_options* opts,
+                   char* out, size_t out_bytes) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, pass, opts, &pl))) return rc;
+  static const char* algos[] = {"auto", "fused", "alternating", "simt"};
+  const auto& lim = frnn::device_limits();
+  char buf[2048];
+  const int n = std::snprintf(
+      buf, sizeof buf,
+      "{\n  \"schema_version\": 1,\n  \"gpu\": \"B200\",\n  \"sm_count\": %d,\n  \"pass\": \"%s\",\n"
+      "  \"shape\": {\"num_states\": %d, \"num_gates\": %d, \"head_dim\": %d, \"num_heads\": %d, "
+      "\"batch\": %d, \"seq_len\": %d, \"dtype\": \"%s\"},\n"
+      "  \"algo\": \"%s\",\n"
+      "  \"tiling\": {\"cluster\": %d, \"units_per_cta\": %d, \"rows_per_cta\": %d, \"batch_tile\": %d, "
+      "\"ctas_per_group\": %d, \"groups\": %d, \"k_split\": %d, \"k_atoms_per_stage\": %d, \"stages\": %d},\n"
+      "  \"grid_blocks\": %d,\n  \"threads_per_block\": %d,\n"
+      "  \"footprint\": {\"smem_bytes\": %d, \"tmem_columns\": %d, \"workspace_bytes\": %lld, "
+      "\"r_matrix_bytes_per_head\": %lld},\n  \"solve_us\": %.1f\n}\n",
+      lim.sm_count, pass == FRNN_PASS_FORWARD ? "forward" : "backward", p.NS, p.NG, p.DH, p.NH, p.B, p.T,
+      p.bf16 ? "bf16" : "fp32", algos[pl.algo & 3], pl.cluster, pl.units_per_cta, pl.rows_per_cta, pl.batch_tile,
+      pl.ctas_per_group, pl.groups, pl.k_split, pl.ka, pl.stages, pl.grid, pl.threads, pl.smem_bytes, pl.tmem_cols,
+      (long long)pl.ws_bytes, (long long)p.NG * p.DH * p.DH * (p.bf16 ? 2 : 4), pl.solve_us);
+  if (!out || n < 0 || (size_t)n + 1 > out_bytes) return fail(FRNN_EINVAL_ARG, "output buffer too small");
+  std::memcpy(out, buf, (size_t)n + 1);
   return FRNN_OK;
 }
 

@@ -138,3 +138,15 @@ def test_partition_rejects_bad_args():
         partition(8, 2, 1, 8, 4, 0)  # more batch shards than rows
     with pytest.raises(abi.FrnnError):
         partition(8, 2, 1, 8, 2, 2)  # rank out of range
+
+
+def test_plan_json_schema():
+    from paper_2412_07752_b200.abi import plan_json
+    j = plan_json("slstm", 1024, 16, 1, 768, "bf16", "backward")
+    assert j["schema_version"] == 1 and j["pass"] == "backward" and j["algo"] == "fused"
+    assert j["shape"] == {"num_states": 4, "num_gates": 4, "head_dim": 768, "num_heads": 1, "batch": 16,
+                          "seq_len": 1024, "dtype": "bf16"}
+    assert j["tiling"]["cluster"] == 16 and j["tiling"]["units_per_cta"] == 48
+    assert j["footprint"]["r_matrix_bytes_per_head"] == 4 * 768 * 768 * 2
+    k = plan_json("slstm", 1024, 64, 1, 3072, "bf16", "backward")
+    assert k["algo"] == "alternating" and k["tiling"]["k_split"] >= 1 and k["tiling"]["stages"] >= 2
