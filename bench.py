@@ -434,6 +434,31 @@ def run_ours(a, rank, world, local_rank):
     e2e = {"value": units * a.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "pipeline": "H2D of step i+1 on a copy stream overlaps step i"}
 
+    # ---- sequential-dependency floor: the same kernels running only
+    # their per-step synchronisation skeleton (h all-gather / partial exchange,
+    # TMEM drains, barriers; no MMAs, no cell math) -- results discarded.
+    floor = None
+    if plan["forward"]["algo"] == 1 and plan["forward"].get("cluster", 0) > 0:
+        L.frnn_debug_skeleton.argtypes = [C.c_int32]
+        L.frnn_debug_skeleton(1)
+        L.frnn_debug_timing(1)
+        step()
+        torch.cuda.synchronize()
+        L.frnn_debug_kernel_ms(None, None)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        L.frnn_debug_kernel_ms(ms3, cnt3)
+        L.frnn_debug_timing(0)
+        L.frnn_debug_skeleton(0)
+        fl_us = [1e3 * ms3[i] / max(1, cnt3[i]) / a.seq for i in range(2)]
+        lat = roof["per_step_latency_us"]
+        floor = {"forward": fl_us[0], "backward": fl_us[1],
+                 "latency_over_floor": {"forward": lat["forward"] / max(1e-9, fl_us[0]),
+                                        "backward": lat["backward"] / max(1e-9, fl_us[1])},
+                 "note": "frnn_debug_skeleton: same cluster kernels, synchronisation only"}
+        roof["sequential_floor_us"] = floor
+
     if rank != 0:
         return
     line = {

@@ -22,6 +22,11 @@ FRNN_API int frnn_debug_profile(void* device_buffer, int32_t steps);
 FRNN_API int frnn_debug_timing(int32_t enable);
 FRNN_API int frnn_debug_kernel_ms(double* ms3, int64_t* count3);
 FRNN_API int frnn_debug_launches(int64_t* count);
+/* 1: the cluster-resident kernels run their synchronisation skeleton only (h
+ * all-gather / partial exchange, TMEM drains, barriers; no MMAs, no cell math):
+ * the per-step floor of the sequential dependency.  Results are
+ * meaningless while enabled. */
+FRNN_API int frnn_debug_skeleton(int32_t enable);
 /* The planner's tiling CSP (algo FRNN_ALGO_FUSED = cluster-resident kernels,
  * FRNN_ALGO_ALTERNATING) for a shape, in the text form of flashrnn_csp.h. */
 FRNN_API int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,

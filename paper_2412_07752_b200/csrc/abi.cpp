@@ -21,6 +21,7 @@
 namespace frnn {
 extern long long* g_prof_buf;
 extern int g_prof_steps;
+extern int g_skeleton;
 }  // namespace frnn
 
 namespace {
@@ -372,6 +373,11 @@ int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, 
   } catch (const std::exception& e) {
     return fail(FRNN_EINVAL_ARG, e.what());
   }
+}
+
+int frnn_debug_skeleton(int32_t enable) {
+  frnn::g_skeleton = enable != 0;
+  return FRNN_OK;
 }
 
 int frnn_debug_profile(void* device_buffer, int32_t steps) {

@@ -30,8 +30,11 @@ struct Math {
     return tanhf(x);
   }
   static __device__ __forceinline__ float l1p(float x) { return FAST ? __logf(1.0f + x) : log1pf(x); }
+  // bf16 mode: sigma(x) = 0.5 + 0.5 tanh(x/2) -- one MUFU op instead of ex2 + rcp
+  // (the pointwise phases are MUFU-throughput bound: 384 threads x 2 elements)
   static __device__ __forceinline__ float sig(float x) {
-    return FAST ? __fdividef(1.0f, 1.0f + __expf(-x)) : 1.0f / (1.0f + expf(-x));
+    if (FAST) return fmaf(0.5f, th(0.5f * x), 0.5f);
+    return 1.0f / (1.0f + expf(-x));
   }
   static __device__ __forceinline__ float logsig(float x) {  // scalar.hpp:64-70
     return x >= 0.f ? -l1p(ex(-x)) : x - l1p(ex(x));
@@ -138,9 +141,12 @@ struct Cell<kSlstm> {
   static __device__ __forceinline__ void fwd(const float* p, const float* g, float* n) {
     // cell.hpp:85-97
     float a = M::logsig(g[1]) + p[3];
-    float m = a > g[2] ? a : g[2];
-    float fexp = M::ex(a - m);
-    float iexp = M::ex(g[2] - m);
+    const bool fa = a > g[2];
+    float m = fa ? a : g[2];
+    // one of exp(a - m), exp(i - m) is exp(0) = 1 exactly: a single MUFU exp
+    const float e = M::ex(fa ? g[2] - a : a - g[2]);
+    float fexp = fa ? 1.f : e;
+    float iexp = fa ? e : 1.f;
     float c = fexp * p[1] + iexp * M::th(g[0]);
     float nn = fexp * p[2] + iexp;
     n[0] = M::sig(g[3]) * (c * M::rcp(nn));
@@ -156,8 +162,9 @@ struct Cell<kSlstm> {
     float a = M::logsig(g[1]) + p[3];
     bool use_a = !(a < g[2]);  // ties -> forget branch (cell.hpp:153)
     float m = use_a ? a : g[2];
-    float fexp = M::ex(a - m);
-    float iexp = M::ex(g[2] - m);
+    const float e = M::ex(use_a ? g[2] - a : a - g[2]);  // the other exponent is exp(0) = 1
+    float fexp = use_a ? 1.f : e;
+    float iexp = use_a ? e : 1.f;
     float tz = M::th(g[0]);
     float c = fexp * p[1] + iexp * tz;
     float n = fexp * p[2] + iexp;

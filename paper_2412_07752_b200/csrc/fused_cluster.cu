@@ -39,6 +39,7 @@ namespace frnn {
 
 extern long long* g_prof_buf;
 extern int g_prof_steps;
+int g_skeleton = 0;  // frnn_debug_skeleton
 
 namespace {
 
@@ -63,6 +64,8 @@ struct CArgs {
   long long* prof;
   int prof_steps;
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
+  int skeleton;    // 1: synchronisation skeleton only -- no MMAs, no cell math (the sequential-
+                   //    dependency floor of SURVEY 8d; frnn_debug_skeleton, results are garbage)
 };
 
 #define FRNN_PROF(slot, step)                                              \
@@ -70,6 +73,8 @@ struct CArgs {
     a.prof[((size_t)blockIdx.x * a.prof_steps + (step)) * 8 + (slot)] = clock64();
 
 __device__ __forceinline__ float bf(const bf16* p, size_t i) { return __bfloat162float(p[i]); }
+__host__ __device__ constexpr int xs_row(int r) { return r + 4 * (r >> 5); }
+__host__ __device__ constexpr int xs_pitch(int rows) { return (xs_row(rows - 1) + 1 + 3) & ~3; }
 __device__ __forceinline__ float lo16(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float hi16(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 __device__ __forceinline__ uint32_t ld2(const bf16* p, size_t i) { return *reinterpret_cast<const uint32_t*>(p + i); }
@@ -96,7 +101,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   const int nb = min(N, p.B - b0);
   const int unit0 = me * a.UPC;
   const int DH = p.DH, D = p.D, B = p.B, K = a.K, T = p.T;
-  const int ROWS = a.R1 + a.R2, XP = ROWS + 1;
+  // xs[b][row'] with row' = row + 4*(row/32): a pad of 4 words per 32 rows makes
+  // both the TMEM drain (consecutive rows) and the pointwise float4 reads (8
+  // consecutive rows per thread) bank-conflict free.
+  const int ROWS = a.R1 + a.R2, XP = xs_pitch(ROWS);
   const bf16* R = static_cast<const bf16*>(p.R);
   const bf16* bias = static_cast<const bf16*>(p.bias);
   const bf16* x = static_cast<const bf16*>(p.x);
@@ -207,11 +215,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       FRNN_PROF(1, t);
       tc_fence_after();
       const uint64_t bd = sdesc_kmajor(smem_u32(buf ? hB1 : hB0), LBO, SBO);
-      if (a.R2)
+      if (a.skeleton) {
+      } else if (a.R2) {
         mma_chain_ts_ss(tbase + a.acc1, tbase, 8, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
                         (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, K / 16);
-      else
+      } else {
         mma_chain_ts(tbase + a.acc1, tbase, 8, bd, (2 * LBO) >> 4, idesc1, K / 16);
+      }
       if (elect_one()) mma_commit(&bars[0]);
       __syncwarp();
     }
@@ -241,34 +251,53 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc1, v);
       if (32 * w + l < a.R1) {
 #pragma unroll
-        for (int n = 0; n < N; ++n) xs[n * XP + 32 * w + l] = v[n];
+        for (int n = 0; n < N; ++n) xs[n * XP + xs_row(32 * w + l)] = v[n];
       }
       if (a.R2) {  // M=64 layout: rows 16w..16w+15 in lanes 32w..32w+15
         tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc2, v);
         if (l < 16 && 16 * w + l < a.R2) {
 #pragma unroll
-          for (int n = 0; n < N; ++n) xs[n * XP + a.R1 + 16 * w + l] = v[n];
+          for (int n = 0; n < N; ++n) xs[n * XP + xs_row(a.R1 + 16 * w + l)] = v[n];
         }
       }
     }
     tc_fence_before();
     __syncthreads();
+    FRNN_PROF(5, t);
     float gout[NG][2], nout[NS][2];
     if (own) {
+      float y[2][4];  // the pair's 2*NGP consecutive gate rows at column b
+      if (NGP == 4) {
+        const float4 y0 = *reinterpret_cast<const float4*>(xs + b * XP + xs_row(u * 4));
+        const float4 y1 = *reinterpret_cast<const float4*>(xs + b * XP + xs_row(u * 4 + 4));
+        y[0][0] = y0.x, y[0][1] = y0.y, y[0][2] = y0.z, y[0][3] = y0.w;
+        y[1][0] = y1.x, y[1][1] = y1.y, y[1][2] = y1.z, y[1][3] = y1.w;
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < NG; ++j) y[h][j] = xs[b * XP + xs_row((u + h) * NGP + j)];
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float g[4], prev[4], nx[4];
 #pragma unroll
         for (int j = 0; j < NG; ++j) {  // x, then b, then y (engine.hpp:183-187)
-          g[j] = (h ? hi16(xr[j]) : lo16(xr[j])) + bj[j][h] + xs[b * XP + (u + h) * NGP + j];
+          g[j] = (h ? hi16(xr[j]) : lo16(xr[j])) + bj[j][h] + y[h][j];
           gout[j][h] = g[j];
         }
 #pragma unroll
         for (int s = 0; s < NS; ++s) prev[s] = st[s][h];
-        C::template fwd<M>(prev, g, nx);
+        if (a.skeleton) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s) nx[s] = g[s & 3];
+        } else {
+          C::template fwd<M>(prev, g, nx);
+        }
 #pragma unroll
         for (int s = 0; s < NS; ++s) st[s][h] = nout[s][h] = nx[s];
       }
+      FRNN_PROF(6, t);
       *reinterpret_cast<uint32_t*>(hs + kmaj(b, u, N)) =
           b < nb ? pack_bf16(nout[0][0], nout[0][1]) : 0u;  // padding rows stay zero
     }
@@ -281,6 +310,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         reinterpret_cast<uint4*>(gst)[i] = reinterpret_cast<const uint4*>(hs)[i];
       fence_proxy_async_global();
       __syncthreads();
+      FRNN_PROF(7, t);
       if (tid == 0) {
         mbar_arrive_expect_tx(&bars[1 + buf], (uint32_t)a.CL * a.slice);  // re-arm for step t+2
         fence_proxy_async_global();
@@ -474,7 +504,33 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       ds[0][1] += t1;
     }
   };
+  auto absorb_rows = [&](int s) {  // DSMEM mode 2: recv[s&1] is [src][n][cu], like the global staging
+    const int pb = s & 1;
+    if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
+    mbar_wait_cluster(&bars[2 + pb], (par_phase >> pb) & 1u);
+    par_phase ^= 1u << pb;
+    if (own) {
+      const float* rp = (pb ? recv1 : recv) + (size_t)b * a.UPC + u;
+      const size_t qs = (size_t)N * a.UPC;
+      float t0 = 0.f, t1 = 0.f;
+      for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
+        const float2 v = *reinterpret_cast<const float2*>(rp + q * qs);
+        t0 += v.x;
+        t1 += v.y;
+      }
+      if (p.clip_mode == 1) {
+        t0 = fminf(fmaxf(t0, -mag), mag);
+        t1 = fminf(fmaxf(t1, -mag), mag);
+      }
+      ds[0][0] += t0;
+      ds[0][1] += t1;
+    }
+  };
   auto absorb = [&](int s) {
+    if (a.dsm == 2) {
+      absorb_rows(s);
+      return;
+    }
     if (dsm) {
       absorb_dsm(s);
       return;
@@ -532,7 +588,14 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         dsl[0] += h ? hi16(hv) : lo16(hv);  // engine.hpp:258-263
 #pragma unroll
         for (int j = 0; j < NG; ++j) g[j] = h ? hi16(gv[j]) : lo16(gv[j]);
-        C::template bwd<M>(prev, g, dsl, dg, dsp);
+        if (a.skeleton) {
+#pragma unroll
+          for (int j = 0; j < NG; ++j) dg[j] = g[j] * dsl[0];
+#pragma unroll
+          for (int s = 0; s < NS; ++s) dsp[s] = dsl[s];
+        } else {
+          C::template bwd<M>(prev, g, dsl, dg, dsp);
+        }
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
           const float d = b < nb ? dg[j] : 0.f;
@@ -563,11 +626,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         const uint64_t ad = sdesc_kmajor(smem_u32(AS), 128 * 16, 128);
         const int nk = KBP / 16, cb = KBP / 2;
         for (int mb = 0; mb < MB; ++mb) {
-          if (mb < MBT)
+          if (a.skeleton) {
+          } else if (mb < MBT) {
             mma_chain_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
-          else
+          } else {
             mma_chain_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)),
                          (2 * 128 * 16) >> 4, bd, (2 * LBO) >> 4, idesc, nk);
+          }
           if (elect_one()) mma_commit(&blkbar[mb]);
           __syncwarp();
         }
@@ -586,7 +651,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + mb * N, v);
         if (c < DH) {
           const int q = c / a.UPC, cu = c % a.UPC;
-          if (dsm) {  // push straight into the owner's recv[t&1][me][cu][:], completing bytes on its mbarrier
+          if (a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
+                             // 32 consecutive columns = one contiguous 128-byte row segment per n
+            const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * a.UPC + cu) * 4), q);
+            const uint32_t mbr = mapa_shared(rbar, q);
+#pragma unroll
+            for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * a.UPC * 4), v[n], mbr);
+          } else if (dsm) {  // push straight into the owner's recv[t&1][me][cu][:], completing bytes on its mbarrier
             const uint32_t dst = mapa_shared(rb + (uint32_t)(((me * a.UPC + cu) * N) * 4), q);
             const uint32_t mbr = mapa_shared(rbar, q);
 #pragma unroll
@@ -676,7 +747,7 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
     s.acc1 = (uint32_t)align_up(s.K / 2, 32);
     s.acc2 = s.acc1 + N;
     s.tmem_cols = pow2_cols(s.acc2 + N);
-    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : 0) + (size_t)N * (rows + 1) * 4 +
+    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : 0) + (size_t)N * xs_pitch(rows) * 4 +
              align_up(s.slice, 16) + 64;
     s.ws = align_up((size_t)s.groups * 2 * s.CL * s.slice, 256);
   } else {
@@ -689,8 +760,9 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
              (size_t)p.NG * N * UPC * 4 + 128;  // + 4 exchange and 8 block mbarriers, TMEM base
     // DSMEM exchange: a second (parity) receive buffer + the summed-term tile
     const size_t dsm_smem = s.smem + (size_t)s.CL * N * UPC * 4 + (size_t)N * (UPC + 2) * 4;
-    const char* xe = getenv("FRNN_XCHG");  // A/B hook: 0 = global + TMA bulk load
+    const char* xe = getenv("FRNN_XCHG");  // A/B hook: 0 = global + TMA bulk load, 1 = DSMEM v4 [cu][n], 2 = rows
     s.dsm = (!xe || atoi(xe) != 0) && dsm_smem <= (size_t)kSmemOptin && (UPC % 4) == 0;
+    if (s.dsm) s.dsm = xe ? atoi(xe) : 2;
     if (s.dsm) s.smem = dsm_smem;
     s.ws = align_up((size_t)s.groups * 2 * s.CL * s.CL * N * UPC * 4, 256);
   }
@@ -721,7 +793,8 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.slice = cs.slice;
   a.prof = g_prof_buf;
   a.prof_steps = g_prof_steps;
-  a.dsm = backward && cs.dsm;
+  a.dsm = backward ? cs.dsm : 0;
+  a.skeleton = g_skeleton;
   char* w = static_cast<char*>(ws);
   if (!backward) {
     a.xstage = reinterpret_cast<bf16*>(w);

@@ -110,7 +110,8 @@ Builder cluster_csp(const Problem& p, int pass, const DeviceLimits& lim, int thr
   if (pass == 0) {
     // SMEM: double-buffered h tile [N x DH], SMEM A block, fp32 accumulator
     // staging [N][rows+1], own h slice, barriers (fused_cluster.cu cluster_shape)
-    b.le(A2P * (DH * 2) + UPC * (N * NGP * 4 + N * 2) + (4 * N * DH + N * 4 + 64),
+    // (the accumulator staging pitch is rows + 4 per 32 rows, rounded to 4 words: <= 9/8 rows + 4)
+    b.le(A2P * (DH * 2) + UPC * (N * NGP * 4 + N * NGP / 2 + N * 2) + (4 * N * DH + N * 16 + 64),
          lim.smem_optin + DH * 2);
     // TMEM: R slice as bf16 pairs (DH/2 columns, 32-aligned) + two N-wide accumulators
     b.le(b.k(((DH / 2 + 31) / 32) * 32 + 2 * N), lim.tmem_cols);

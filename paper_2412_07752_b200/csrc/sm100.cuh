@@ -458,6 +458,11 @@ __device__ __forceinline__ void st_async_v4(uint32_t dst, float a, float b, floa
                : "memory");
 }
 
+__device__ __forceinline__ void st_async_b32(uint32_t dst, float a, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+               "r"(__float_as_uint(a)), "r"(mbar)
+               : "memory");
+}
 __device__ __forceinline__ void st_async_v4_b32(uint32_t dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                                 uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
