@@ -17,12 +17,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "libflashrnn.so")
+OBJ = os.path.join(ROOT, "build", os.environ.get("FRNN_BUILD_TAG", "obj"))
+LIB = os.environ.get("FRNN_BUILD_LIB", os.path.join(PKG, "libflashrnn.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"] + os.environ.get("FRNN_EXTRA_FLAGS", "").split()
 
 
 def _sources():

@@ -185,11 +185,13 @@ __global__ void __launch_bounds__(ATHREADS, 1)
         if (lr) load_r(kb, s.stage0 + kb * a.stage_bytes, &s.full[kb]);
       }
       griddep_wait();
+      ALT_PROF(5);
       for (int kb = 0; kb < npre; ++kb)
         if (lh) load_h(kb, s.stage0 + kb * a.stage_bytes, &s.full[kb]);
       for (int kb = npre; kb < a.numk; ++kb) {
         const int st = kb % a.stages;
         mbar_wait(&s.empty[st], ((kb / a.stages) - 1) & 1);
+        if (kb == npre) ALT_PROF(6);
         uint8_t* sp = s.stage0 + st * a.stage_bytes;
         mbar_arrive_expect_tx(&s.full[st], sb);
         if (lr) load_r(kb, sp, &s.full[st]);
@@ -215,8 +217,12 @@ __global__ void __launch_bounds__(ATHREADS, 1)
           }
         }
       }
-      if (elect_one()) mma_commit(&s.empty[st]);
+      if (elect_one()) {
+        if (a.dbg & 8) mbar_arrive(&s.empty[st]);  // experiment: plain arrive (valid only without MMAs)
+        else mma_commit(&s.empty[st]);
+      }
       __syncwarp();
+      if (kb == 0) ALT_PROF_BY(7, 32);
     }
     if (elect_one()) mma_commit(s.done);
     __syncwarp();

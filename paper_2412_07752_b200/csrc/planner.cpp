@@ -164,11 +164,15 @@ Builder alt_csp(const Problem& p, int pass, const DeviceLimits& lim) {
     b.le(NB * ((DH + UPT - 1) / UPT * p.NH), std::max(lim.sm_count, (DH + UPT - 1) / UPT * p.NH));
     b.prefer("NB", Pref::Smallest);
   } else {
-    auto KS = b.var("KS", Domain::span(1, kAltMaxKS));
+    const int ks_cap = getenv("FRNN_ALT_KS") ? std::max(1, atoi(getenv("FRNN_ALT_KS"))) : kAltMaxKS;  // experiments
+    auto KS = b.var("KS", Domain::span(1, std::min(ks_cap, kAltMaxKS)));
     b.le(KS, KPG * std::max(1, nrec));                            // every rank has K blocks
     if (nrec == 0) b.eq(KS, 1);
     b.le(N * 528 + 2048, lim.smem_optin);                         // epilogue [N][132] fp32
-    b.le(KS * NB * ((DH + 127) / 128 * p.NH), std::max(lim.sm_count, (DH + 127) / 128 * p.NH));
+    // one wave that leaves a third of the SMs free: the next step's CTAs (PDL) become
+    // resident and prefetch R while this step drains (measured at H=3072: 96 CTAs
+    // 27 us/step, 144 CTAs 42 us/step -- profiles/r01_alt_ks_sweep_c5.txt)
+    b.le(KS * NB * ((DH + 127) / 128 * p.NH), std::max(lim.sm_count * 2 / 3, (DH + 127) / 128 * p.NH));
     b.prefer("NB", Pref::Smallest);
     b.prefer("KS", Pref::Largest);  // spread the per-step R^T stream over the SMs
   }

@@ -256,12 +256,44 @@ __device__ __forceinline__ bool mbar_try_cluster(uint32_t a, uint32_t phase) {
 }
 // try_wait suspends in hardware; after ~4 s without completion the kernel
 // traps (a protocol bug must not hang the GPU).
+// Non-blocking probes (test_wait never suspends the thread).
+__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test_cluster(uint32_t a, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 "
+      "%0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+#ifdef FRNN_TRYWAIT  // A/B build: suspend in try_wait instead of spinning on test_wait
+constexpr bool g_spin_wait = false;
+#else
+constexpr bool g_spin_wait = true;
+#endif
+// Waits are on the per-step critical path: spin with test_wait (a suspended
+// try_wait wakes up late, ~0.2-0.5 us); after ~4 s without completion the
+// kernel traps (a protocol bug must not hang the GPU).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try(a, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_sleep(a, phase, 1000000u))
-    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+  uint32_t n = 0;
+  while (!(g_spin_wait ? mbar_test(a, phase) : mbar_try_sleep(a, phase, 1000000u)))
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -354,8 +386,9 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
   const uint32_t a = smem_u32(bar);
   if (mbar_try_cluster(a, phase)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_cluster_sleep(a, phase, 1000000u))
-    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+  uint32_t n = 0;
+  while (!(g_spin_wait ? mbar_test_cluster(a, phase) : mbar_try_cluster_sleep(a, phase, 1000000u)))
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
 }
 // Arrive (count 1) on the mbarrier at cluster-shared address `remote`.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t remote) {

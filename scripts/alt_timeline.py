@@ -52,8 +52,14 @@ def timeline(name, grid, run):
         dn = [c[2] for c in v[k]]
         en = [c[3] for c in v[k]]
         pr = [c[4] for c in v[k]]
+        p5 = [c[5] for c in v[k]]
+        p6 = [c[6] for c in v[k]]
+        p7 = [c[7] for c in v[k]]
         rows.append(dict(s0=min(st), s1=max(st), r0=min(rel), r1=max(rel), d=S.median([d - r for d, r in zip(dn, rel)]),
                          prod=S.median([q - r for q, r in zip(pr, rel)]) if min(pr) > 0 else -1,
+                         p5=S.median([q - r for q, r in zip(p5, rel)]) if min(p5) > 0 else -1,
+                         p6=S.median([q - r for q, r in zip(p6, p5)]) if min(p6) > 0 else -1,
+                         p7=S.median([q - r for q, r in zip(p7, p5)]) if min(p7) > 0 else -1,
                          dmax=max(d - r for d, r in zip(dn, rel)), ep=S.median([e - d for e, d in zip(en, dn)]),
                          e1=max(en), e0=min(en)))
     print(f"== {name}: grid {grid}, ns")
@@ -61,7 +67,7 @@ def timeline(name, grid, run):
     for k in range(1, a.steps):
         p, c = rows[k - 1], rows[k]
         print(f" {k:4d}  {c['s0'] - p['e1']:8d}  {c['r0'] - p['e1']:8d}  {c['r1'] - c['r0']:8d}  {c['prod']:8.0f}  {c['d']:7.0f}/{c['dmax']:7.0f}  {c['ep']:7.0f}  {c['e1'] - c['s0']:8d}"
-              f"  step period {c['e1'] - p['e1']}")
+              f"  step period {c['e1'] - p['e1']}  producer release->own wait {c['p5']:.0f}  first empty wait {c['p6']:.0f}  mma warp stage-0 done after release {c['p7']:.0f}")
 
 
 pf = eng.plan(a.variant, a.seq, a.batch, 1, DH, "bf16", "forward")
