@@ -174,21 +174,22 @@ def _ref_worker(args):
     return time.perf_counter() - t0
 
 
-def cpu_reference_step(a, T_sample, pool, cores):
-    """One bounded sample of the workload on the host: the a.batch rows are
+def cpu_reference_step(a, T_sample, pool, cores, B=None):
+    """One bounded sample of the workload on the host: the B rows are
     independent (engine.hpp:173, only dR/db sum over b), so each row is one
     reference call in its own process; returns (B*T/s, wall seconds)."""
-    jobs = [(a.variant, T_sample, a.hidden // a.heads, a.heads, 1000 + r) for r in range(a.batch)]
+    B = a.batch if B is None else B
+    jobs = [(a.variant, T_sample, a.hidden // a.heads, a.heads, 1000 + r) for r in range(B)]
     t0 = time.perf_counter()
     list(pool.map(_ref_worker, jobs))
     wall = time.perf_counter() - t0
-    return a.batch * T_sample / wall, wall
+    return B * T_sample / wall, wall
 
 
-def make_pool(a):
+def make_pool(a, B=None):
     import concurrent.futures as cf
     import multiprocessing as mp
-    cores = max(1, min(os.cpu_count() or 1, a.batch))
+    cores = max(1, min(os.cpu_count() or 1, a.batch if B is None else B))
     return cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork")), cores
 
 
@@ -229,28 +230,31 @@ def run_reference(a, rank, world):
     if not O.Reference.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref.so missing"}), flush=True)
         return
-    pool, cores = make_pool(a)
-    T_s = a.cpu_sample_steps
+    # the same workload as our arm: B = batch_per_gpu x world rows (weak scaling),
+    # each step a bounded T sample (shortened as rows grow, so the run stays minutes long)
+    B = a.batch * world
+    pool, cores = make_pool(a, B)
+    T_s = max(8, a.cpu_sample_steps // world)
     try:
         for _ in range(a.warmup):
-            cpu_reference_step(a, max(2, T_s // 8), pool, cores)
+            cpu_reference_step(a, max(2, T_s // 8), pool, cores, B)
         walls = []
         for _ in range(a.steps):
-            _, w = cpu_reference_step(a, T_s, pool, cores)
+            _, w = cpu_reference_step(a, T_s, pool, cores, B)
             walls.append(w)
     finally:
         pool.shutdown()
     total = sum(walls)
-    value = a.batch * T_s * a.steps / total
+    value = B * T_s * a.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (numpy RNG, reference distributions)",
-        "config": {"workload": workload_name(a), "batch_per_gpu": a.batch, "seq_len": a.seq,
+        "config": {"workload": workload_name(a), "batch_per_gpu": a.batch, "global_batch": B, "seq_len": a.seq,
                    "hidden": a.hidden, "heads": a.heads, "sample_seq_len": T_s},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"B={a.batch} rows x T={T_s} steps per step, engine<float>",
+                         "sample": f"B={B} rows x T={T_s} steps per step, engine<float>",
                          "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -488,6 +492,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: FRNN_BENCH_SHARE_GPU=1 maps every rank onto cuda:0 with gloo
+    # collectives, to exercise the N>1 code path on a single-GPU box
+    share = os.environ.get("FRNN_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     if a.impl == "reference":
         run_reference(a, rank, world)
         return
@@ -495,7 +504,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(a, rank, world, local_rank)
     finally:
