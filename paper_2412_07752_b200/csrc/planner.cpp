@@ -152,7 +152,8 @@ Builder alt_csp(const Problem& p, int pass, const DeviceLimits& lim) {
   const int ring = getenv("FRNN_ALT_SMEM_KB") ? atoi(getenv("FRNN_ALT_SMEM_KB")) * 1024 : 200 * 1024;
   auto N = b.var("N", Domain::grid(16, 128, 16));
   auto NB = b.var("NB", Domain::span(1, (p.B + 15) / 16));
-  auto KA = b.var("KA", Domain::span(1, 2));
+  const int ka_max = getenv("FRNN_ALT_KA_MAX") ? std::max(1, atoi(getenv("FRNN_ALT_KA_MAX"))) : 4;  // experiments
+  auto KA = b.var("KA", Domain::span(1, ka_max));
   auto KPG = b.var("KPG", Domain::span(1, std::max(1, DH / 64)));
   auto ST = b.var("ST", Domain::span(2, 8));
   b.le(p.B, N * NB);
