@@ -15,6 +15,7 @@
 #include "rnnkit/rnn/gradcheck.hpp"
 #include "rnnkit/rnn/random_init.hpp"
 #include "rnnkit/rnn/tensor_io.hpp"
+#include "rnnkit/tasks/parity.hpp"
 
 using namespace rnnkit::rnn;
 
@@ -173,6 +174,30 @@ int ref_save_case(const char* path, int v, int T, int B, int NH, int DH, uint64_
     t["d_recurrent"] = NamedTensor{{(uint64_t)NH, NG, (uint64_t)DH, (uint64_t)DH}, g.d_recurrent};
     t["d_init_states"] = NamedTensor{{NS, (uint64_t)B, D}, g.d_init_states};
     save_tensors(path, t);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// The reference parity-task trainer (parity.cpp:142-245), in double on the CPU.
+int ref_train_parity(int v, int dh, int nh, int steps, int batch, int len_max, int warmup, double lr, uint64_t seed,
+                     int eval_sequences, int eval_len_min, int eval_len_max, double* losses, int* steps_run,
+                     double* final_acc) {
+  try {
+    rnnkit::tasks::ParityConfig cfg;
+    cfg.steps = steps;
+    cfg.batch_size = batch;
+    cfg.train_len_max = len_max;
+    cfg.warmup_steps = warmup;
+    cfg.eval_every = 0;
+    cfg.eval_sequences = eval_sequences;
+    cfg.eval_len_min = eval_len_min;
+    cfg.eval_len_max = eval_len_max;
+    auto run = rnnkit::tasks::train_parity_run(static_cast<Variant>(v), dh, nh, cfg, lr, seed);
+    for (size_t i = 0; i < run.losses.size(); ++i) losses[i] = run.losses[i];
+    *steps_run = run.steps_run;
+    *final_acc = run.final_accuracy;
     return 0;
   } catch (const std::exception&) {
     return -1;
