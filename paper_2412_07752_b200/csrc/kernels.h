@@ -94,6 +94,12 @@ cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_
 size_t alt_forward_ws(const Problem& p, const Plan& pl);
 size_t alt_backward_ws(const Problem& p, const Plan& pl);
 
+// ---- fp32 mode beyond shared-memory R (alt_fp32.cu) ----
+cudaError_t alt32_forward(const Problem& p, void* ws, cudaStream_t s);
+cudaError_t alt32_backward(const Problem& p, void* ws, cudaStream_t s);
+size_t alt32_forward_ws(const Problem& p);
+size_t alt32_backward_ws(const Problem& p);
+
 // ---- parameter gradients dR / db (param_grads.cu) ----
 // dg element (t, b, j, e) lives at dg[t*ts + b*bs + j*js + e].
 struct DgView {

@@ -355,12 +355,26 @@ std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimi
 }
 
 int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Plan* out, std::string* why) {
-  if (!p.bf16) {
-    if (algo != FRNN_ALGO_AUTO && algo != FRNN_ALGO_SIMT) {
-      *why = "fp32 mode runs on the SIMT (FFMA) kernels only";
+  if (!p.bf16) {  // fp32 parity mode: FFMA kernels (no fp32 tensor-core path meets rel 1e-5)
+    if (algo == FRNN_ALGO_FUSED) {
+      *why = "fp32 mode runs on the FFMA kernels (simt or alternating)";
       return FRNN_EUNSUPPORTED;
     }
-    return plan_simt(p, pass, lim, out, why) ? FRNN_OK : FRNN_EINFEASIBLE;
+    if (algo != FRNN_ALGO_ALTERNATING && plan_simt(p, pass, lim, out, why)) return FRNN_OK;
+    if (algo == FRNN_ALGO_SIMT) return FRNN_EINFEASIBLE;
+    Plan& pl = *out;  // R streamed through shared memory every step (alt_fp32.cu)
+    pl = Plan{};
+    pl.algo = FRNN_ALGO_ALTERNATING;
+    pl.rows_per_cta = 32;
+    pl.batch_tile = 16;
+    pl.units_per_cta = pass == 0 ? 32 / (p.NG == 1 ? 1 : 4) : 32;
+    pl.ctas_per_group = 1;
+    pl.groups = ((p.DH + pl.units_per_cta - 1) / pl.units_per_cta) * p.NH * ((p.B + 15) / 16);
+    pl.grid = pl.groups;
+    pl.threads = 256;
+    pl.k_split = 1;
+    pl.ws_bytes = pass == 0 ? alt32_forward_ws(p) : alt32_backward_ws(p);
+    return FRNN_OK;
   }
   if (algo == FRNN_ALGO_SIMT) {
     *why = "bf16 mode has no SIMT path";

@@ -138,6 +138,26 @@ def test_fp32_golden(eng):
 
 # ------------------------------------------------------------- bf16 mode ----
 @pytest.mark.parametrize("v", VARIANTS)
+@pytest.mark.parametrize("clip,mag", [("off", 0.0), ("value", 0.05), ("zero", 0.0)])
+def test_fp32_beyond_shared_memory(eng, orc, v, clip, mag):
+    """fp32 mode with R too large for the SIMT kernels' shared memory (DH=128,
+    two heads, ragged batch): the streamed FFMA path (alt_fp32.cu), rel 1e-5."""
+    inp = orc.generate(v, 6, 19, 2, 128, seed=12)
+    dh = np.random.RandomState(4).randn(6, 19, 256)
+    if v != "elman":  # a single-gate R still fits the SIMT kernels at DH=128
+        assert eng.plan(v, 6, 19, 2, 128, "f32", "backward")["algo"] == 2
+    gpu = run_gpu(eng, v, inp, False, clip, mag, dh, algo="alternating")
+    assert_close(gpu, run_oracle(orc, v, inp, False, clip, mag, dh), FP32_TOL)
+
+
+@pytest.mark.parametrize("v", ["lstm", "slstm"])
+def test_fp32_h768(eng, orc, v):
+    """fp32 mode at the headline shape (B=16, H=768, NH=1), reduced T."""
+    inp = orc.generate(v, 4, 16, 1, 768, seed=13)
+    assert_close(run_gpu(eng, v, inp, False), run_oracle(orc, v, inp, False), FP32_TOL)
+
+
+@pytest.mark.parametrize("v", VARIANTS)
 def test_bf16_fused_h768(eng, orc, v):
     """Configs 2/4 shape (H=768, NH=1, B=16) at reduced T (oracle cost)."""
     inp = orc.generate(v, 24, 16, 1, 768, seed=0)

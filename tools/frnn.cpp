@@ -6,7 +6,7 @@
 //   frnn feasible-heads  --variant V [--min 16 --max 1024 --step 16 --heads 1 --batch 16]
 //   frnn solve-csp       <problem.txt>          (text form of include/flashrnn_csp.h)
 //   frnn gradcheck       --variant V [--t 8 --dh 16 --heads 2 --batch 4 --seeds 1 --h 1e-2 --floor 0.1 --tol 1e-2]
-//   frnn precision-drift --variant V [--t 512 --dh 64 --heads 12 --batch 1]
+//   frnn precision-drift --variant V [--t 512 --dh 768 --heads 1 --batch 1]
 //   frnn train-parity    --variant V [--dh 16 --heads 1 --steps N --batch 64 --train-len-max 40
 //                         --warmup W --eval-every E --eval-sequences S --lrs a,b --seeds 1,2]
 //   common: --seed S, --json, --out FILE
@@ -21,8 +21,7 @@
 // pinned against the f64 oracle to 1e-5 normwise by tests/test_gpu_parity.py.
 // precision-drift compares the GPU bf16 forward with the GPU fp32 forward of
 // the same inputs (engine.cpp:45-71 uses the double engine as the
-// high-precision side; fp32 is within 1e-6 of it).  The fp32 kernels keep a
-// head's R in shared memory, so drift runs use multi-head shapes (DH <= ~100).
+// high-precision side; fp32 is within 1e-6 of it).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -237,7 +236,7 @@ int cmd_gradcheck(const Args& a) {
 // ------------------------------------------------------- precision drift --
 int cmd_precision_drift(const Args& a) {
   const auto cell = rnn::cell_spec(variant_of(a));
-  const int T = (int)a.num("t", 512), dh = (int)a.num("dh", 64), nh = (int)a.num("heads", 12),
+  const int T = (int)a.num("t", 512), dh = (int)a.num("dh", 768), nh = (int)a.num("heads", 1),
             B = (int)a.num("batch", 1);
   rnn::Rng rng((std::uint64_t)a.num("seed", 0));
   const auto pd = rnn::random_params(cell, nh, dh, rng);
