@@ -203,13 +203,15 @@ int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32
       "\"batch\": %d, \"seq_len\": %d, \"dtype\": \"%s\"},\n"
       "  \"algo\": \"%s\",\n"
       "  \"tiling\": {\"cluster\": %d, \"units_per_cta\": %d, \"rows_per_cta\": %d, \"batch_tile\": %d, "
-      "\"ctas_per_group\": %d, \"groups\": %d, \"k_split\": %d, \"k_atoms_per_stage\": %d, \"stages\": %d},\n"
+      "\"ctas_per_group\": %d, \"groups\": %d, \"k_split\": %d, \"k_atoms_per_stage\": %d, \"stages\": %d, "
+      "\"step_kernels\": \"%s\"},\n"
       "  \"grid_blocks\": %d,\n  \"threads_per_block\": %d,\n"
       "  \"footprint\": {\"smem_bytes\": %d, \"tmem_columns\": %d, \"workspace_bytes\": %lld, "
       "\"r_matrix_bytes_per_head\": %lld},\n  \"solve_us\": %.1f\n}\n",
       lim.sm_count, pass == FRNN_PASS_FORWARD ? "forward" : "backward", p.NS, p.NG, p.DH, p.NH, p.B, p.T,
       p.bf16 ? "bf16" : "fp32", algos[pl.algo & 3], pl.cluster, pl.units_per_cta, pl.rows_per_cta, pl.batch_tile,
-      pl.ctas_per_group, pl.groups, pl.k_split, pl.ka, pl.stages, pl.grid, pl.threads, pl.smem_bytes, pl.tmem_cols,
+      pl.ctas_per_group, pl.groups, pl.k_split, pl.ka, pl.stages,
+      pl.algo == FRNN_ALGO_SIMT ? "simt" : (pl.ffma || !p.bf16) ? "ffma" : "tcgen05", pl.grid, pl.threads, pl.smem_bytes, pl.tmem_cols,
       (long long)pl.ws_bytes, (long long)p.NG * p.DH * p.DH * (p.bf16 ? 2 : 4), pl.solve_us);
   if (!out || n < 0 || (size_t)n + 1 > out_bytes) return fail(FRNN_EINVAL_ARG, "output buffer too small");
   std::memcpy(out, buf, (size_t)n + 1);

@@ -699,13 +699,13 @@ bool alt_supported(const Problem& p, std::string* why) {
   return true;
 }
 
-size_t alt_forward_ws(const Problem& p, const Plan&) {
-  if (!p.bf16) return alt32_forward_ws(p);
+size_t alt_forward_ws(const Problem& p, const Plan& pl) {
+  if (!p.bf16 || pl.ffma) return alt32_forward_ws(p);
   return align_up(sizeof(float) * (size_t)p.NS * p.B * p.D, 256);
 }
 
 size_t alt_backward_ws(const Problem& p, const Plan& pl) {
-  if (!p.bf16) return alt32_backward_ws(p);
+  if (!p.bf16 || pl.ffma) return alt32_backward_ws(p);
   size_t off = align_up(sizeof(float) * (size_t)p.NS * p.B * p.D, 256);
   if (!all_inputs(p)) off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
   const int N = pl.batch_tile > 0 ? pl.batch_tile : 16;
@@ -714,7 +714,7 @@ size_t alt_backward_ws(const Problem& p, const Plan& pl) {
 }
 
 cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t st) {
-  if (!p.bf16) return alt32_forward(p, ws, st);
+  if (!p.bf16 || pl.ffma) return alt32_forward(p, ws, st);
   std::string why;
   if (!alt_supported(p, &why) || !tmap_encoder()) return cudaErrorNotSupported;
   const AltShape sh = alt_shape(p, false, pl.batch_tile, 1, pl.ka, pl.stages);
@@ -767,7 +767,7 @@ cudaError_t alt_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t
 }
 
 cudaError_t alt_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t st) {
-  if (!p.bf16) return alt32_backward(p, ws, st);
+  if (!p.bf16 || pl.ffma) return alt32_backward(p, ws, st);
   std::string why;
   if (!alt_supported(p, &why) || !tmap_encoder()) return cudaErrorNotSupported;
   const AltShape sh = alt_shape(p, true, pl.batch_tile, pl.k_split, pl.ka, pl.stages);

@@ -36,6 +36,7 @@ struct Plan {
   int grid, threads, smem_bytes, tmem_cols, k_split;
   int cluster;         // >0: cluster-resident fused kernels with this cluster size
   int ka, stages;      // alternating path: K atoms per pipeline stage, ring depth
+  int ffma;            // alternating path on the FFMA step kernels (alt_fp32.cu)
   size_t ws_bytes;
   double solve_us;
 };

@@ -347,6 +347,24 @@ bool plan_simt(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, s
   return true;
 }
 
+// FFMA step kernels (alt_fp32.cu): 32 gate rows / 32 state columns x 16 batch
+// rows per CTA, R streamed through shared memory every step.
+void plan_ffma(const Problem& p, int pass, Plan* out) {
+  Plan& pl = *out;
+  pl = Plan{};
+  pl.algo = FRNN_ALGO_ALTERNATING;
+  pl.ffma = 1;
+  pl.rows_per_cta = 32;
+  pl.batch_tile = 16;
+  pl.units_per_cta = pass == 0 ? 32 / (p.NG == 1 ? 1 : 4) : 32;
+  pl.ctas_per_group = 1;
+  pl.groups = ((p.DH + pl.units_per_cta - 1) / pl.units_per_cta) * p.NH * ((p.B + 15) / 16);
+  pl.grid = pl.groups;
+  pl.threads = 256;
+  pl.k_split = 1;
+  pl.ws_bytes = pass == 0 ? alt32_forward_ws(p) : alt32_backward_ws(p);
+}
+
 }  // namespace
 
 std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimits& lim) {
@@ -362,20 +380,10 @@ int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Pl
     }
     if (algo != FRNN_ALGO_ALTERNATING && plan_simt(p, pass, lim, out, why)) return FRNN_OK;
     if (algo == FRNN_ALGO_SIMT) return FRNN_EINFEASIBLE;
-    Plan& pl = *out;  // R streamed through shared memory every step (alt_fp32.cu)
-    pl = Plan{};
-    pl.algo = FRNN_ALGO_ALTERNATING;
-    pl.rows_per_cta = 32;
-    pl.batch_tile = 16;
-    pl.units_per_cta = pass == 0 ? 32 / (p.NG == 1 ? 1 : 4) : 32;
-    pl.ctas_per_group = 1;
-    pl.groups = ((p.DH + pl.units_per_cta - 1) / pl.units_per_cta) * p.NH * ((p.B + 15) / 16);
-    pl.grid = pl.groups;
-    pl.threads = 256;
-    pl.k_split = 1;
-    pl.ws_bytes = pass == 0 ? alt32_forward_ws(p) : alt32_backward_ws(p);
+    plan_ffma(p, pass, out);
     return FRNN_OK;
   }
+
   if (algo == FRNN_ALGO_SIMT) {
     *why = "bf16 mode has no SIMT path";
     return FRNN_EUNSUPPORTED;
@@ -390,7 +398,13 @@ int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Pl
     }
   }
   if (plan_alt(p, pass, lim, out, &w3)) return FRNN_OK;
-  *why = algo == FRNN_ALGO_AUTO ? w1 + "; " + w2 + "; " + w3 : w3;
+  if (algo == FRNN_ALGO_AUTO || algo == FRNN_ALGO_ALTERNATING) {
+    // no tensor-core tiling for this head dim (not a multiple of 8 / of 64):
+    // bf16 storage on the FFMA step kernels
+    plan_ffma(p, pass, out);
+    return FRNN_OK;
+  }
+  *why = w3;
   return FRNN_EINFEASIBLE;
 }
 

@@ -150,3 +150,8 @@ def test_plan_json_schema():
     assert j["footprint"]["r_matrix_bytes_per_head"] == 4 * 768 * 768 * 2
     k = plan_json("slstm", 1024, 64, 1, 3072, "bf16", "backward")
     assert k["algo"] == "alternating" and k["tiling"]["k_split"] >= 1 and k["tiling"]["stages"] >= 2
+    assert k["tiling"]["step_kernels"] == "tcgen05"
+    # bf16 head dims the tensor-core kernels cannot tile fall to the FFMA step kernels
+    for v, dh in (("lstm", 20), ("gru", 36), ("elman", 1000)):
+        f = plan_json(v, 16, 8, 1, dh, "bf16", "forward")
+        assert f["algo"] == "alternating" and f["tiling"]["step_kernels"] == "ffma"

@@ -228,6 +228,16 @@ def test_alternating_two_batch_tiles(eng, orc):
     check_bf16(eng, orc, "lstm", inp, algo="alternating")
 
 
+@pytest.mark.parametrize("v,NH,DH", [("lstm", 3, 20), ("gru", 2, 36), ("slstm", 1, 12), ("elman", 1, 1000)])
+def test_bf16_untileable_head_dims(eng, orc, v, NH, DH):
+    """bf16 head dims no tensor-core kernel tiles (not a multiple of 8, or past
+    the fused limits and not a multiple of 64): FFMA step kernels, bf16 storage."""
+    T = 4 if DH > 256 else 10
+    inp = orc.generate(v, T, 19, NH, DH, seed=11)
+    dh = np.random.RandomState(5).randn(T, 19, NH * DH)
+    check_bf16(eng, orc, v, inp, dh=dh)
+
+
 def test_alternating_matches_fused(eng, orc):
     """Same inputs through the cluster-resident and the alternating kernels."""
     inp = orc.generate("slstm", 16, 16, 1, 768, seed=8)
