@@ -33,7 +33,8 @@ __global__ void __launch_bounds__(384, 1) bench(int mode, int gap, long long* ou
   __syncthreads();
   tc_fence_after();
   const uint32_t t = tb;
-  const bool per = mode & 1, seq = mode & 2, none = mode & 4, wdg = mode & 8, spin = mode & 16;
+  const bool per = mode & 1, seq = mode & 2, none = mode & 4, wdg = mode & 8, spin = mode & 16, fen = mode & 32,
+             drain = mode & 64;
   const int last = per ? 3 : 0;
   long long dts[ITERS], iss[ITERS];
   for (int it = 0; it < ITERS; ++it) {
@@ -46,7 +47,9 @@ __global__ void __launch_bounds__(384, 1) bench(int mode, int gap, long long* ou
       reinterpret_cast<uint4*>(sm + DGB)[tid] = make_uint4(0x3c003c00u, it, tid, 0x3c003c00u);
       fence_proxy_async_smem();
     }
+    if (fen) tc_fence_before();
     __syncthreads();
+    if (fen) tc_fence_after();
     const long long t0 = clock64();
     if (w == 0) {
       tc_fence_after();
@@ -78,6 +81,15 @@ __global__ void __launch_bounds__(384, 1) bench(int mode, int gap, long long* ou
       for (int i = 0; i < 3; ++i) mbar_wait(&bar[i], it & 1);
     if (spin && w >= 2)  // like the drain warps: everyone waits on the block barriers
       for (int i = 0; i <= last; ++i) mbar_wait(&bar[i], it & 1);
+    if (drain) {  // every warp reads one accumulator block of its lane quadrant, like the drain
+      mbar_wait(&bar[last], it & 1);
+      tc_fence_after();
+      float v[16];
+      tmem_ld16(t + ((uint32_t)(32 * (w & 3)) << 16) + 384 + (w >> 2) * N, v);
+      float acc = 0.f;
+      for (int q = 0; q < 16; ++q) acc += v[q];
+      if (acc == 12345.f) out[31] = 1;
+    }
   }
   if (tid == 0) {
     for (int i = 1; i < ITERS; ++i)
@@ -109,9 +121,9 @@ int main() {
   cudaFuncSetAttribute(bench, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* names[] = {"interleaved, 1 commit", "interleaved, per-pair commits", "sequential, 1 commit",
                          "sequential, per-pair commits", "no MMAs, 1 commit", "no MMAs, 4 commits"};
-  const int modes[] = {0, 1, 5};
+  const int modes[] = {1, 1 | 32, 1 | 64, 1 | 32 | 64, 1 | 8 | 16 | 32 | 64};
   for (int cl : {16})
-    for (int gap : {0, 1000, 3000, 6000, 12000})
+    for (int gap : {0, 3000})
     for (int mode : modes) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(cl);
