@@ -15,19 +15,21 @@
 
 using namespace frnn::sm100;
 
-constexpr int N = 16, KB = 192, ITERS = 64, SMEM = 218432, DGB = 196608;
+constexpr int N = 16, KB = 192, ITERS = 64, SMEM = 218432 + 256, DGB = 196608, BAROFF = 218432;
 
 __global__ void __launch_bounds__(384, 1) bench(int mode, int gap, long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t bar[8];
+  __shared__ uint64_t sbar[8];
+  uint64_t* bar = (mode & 128) ? reinterpret_cast<uint64_t*>(sm + BAROFF) : sbar;  // barriers where the kernel has them
   __shared__ uint32_t tb;
   const int tid = threadIdx.x, w = tid >> 5;
   if (w == 0) tmem_alloc(&tb, 512);
+  for (int i = tid; i < BAROFF / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
+  __syncthreads();
   if (tid == 0) {
     for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < SMEM / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -121,9 +123,9 @@ int main() {
   cudaFuncSetAttribute(bench, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* names[] = {"interleaved, 1 commit", "interleaved, per-pair commits", "sequential, 1 commit",
                          "sequential, per-pair commits", "no MMAs, 1 commit", "no MMAs, 4 commits"};
-  const int modes[] = {1, 1 | 32, 1 | 64, 1 | 32 | 64, 1 | 8 | 16 | 32 | 64};
+  const int modes[] = {1, 5, 1 | 128, 5 | 128, 5 | 16 | 128, 1 | 8 | 16 | 32 | 64 | 128};
   for (int cl : {16})
-    for (int gap : {0, 3000})
+    for (int gap : {0})
     for (int mode : modes) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(cl);
