@@ -18,9 +18,27 @@ namespace frnn {
 
 enum Variant { kElman = 0, kLstm = 1, kGru = 2, kSlstm = 3 };
 
+// Raw MUFU approximations with flush-to-zero: no denormal range fix-ups on the
+// pointwise critical path (bf16 mode only).
+__device__ __forceinline__ float mufu_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <bool FAST>
 struct Math {
-  static __device__ __forceinline__ float ex(float x) { return FAST ? __expf(x) : expf(x); }
+  static __device__ __forceinline__ float ex(float x) { return FAST ? mufu_ex2(x * 1.44269504088896341f) : expf(x); }
   static __device__ __forceinline__ float th(float x) {
     if (FAST) {
       float y;
@@ -29,17 +47,23 @@ struct Math {
     }
     return tanhf(x);
   }
-  static __device__ __forceinline__ float l1p(float x) { return FAST ? __logf(1.0f + x) : log1pf(x); }
+  static __device__ __forceinline__ float l1p(float x) {
+    return FAST ? mufu_lg2(1.0f + x) * 0.693147180559945309f : log1pf(x);
+  }
   // bf16 mode: sigma(x) = 0.5 + 0.5 tanh(x/2) -- one MUFU op instead of ex2 + rcp
   // (the pointwise phases are MUFU-throughput bound: 384 threads x 2 elements)
   static __device__ __forceinline__ float sig(float x) {
     if (FAST) return fmaf(0.5f, th(0.5f * x), 0.5f);
     return 1.0f / (1.0f + expf(-x));
   }
-  static __device__ __forceinline__ float logsig(float x) {  // scalar.hpp:64-70
+  // scalar.hpp:64-70: x >= 0 ? -log1p(e^-x) : x - log1p(e^x).  bf16 mode evaluates
+  // the same split branch-free as min(x, 0) - log1p(e^-|x|) (a divergent branch
+  // would run both sides' MUFU chains back to back).
+  static __device__ __forceinline__ float logsig(float x) {
+    if (FAST) return fminf(x, 0.f) - l1p(ex(-fabsf(x)));
     return x >= 0.f ? -l1p(ex(-x)) : x - l1p(ex(x));
   }
-  static __device__ __forceinline__ float rcp(float x) { return FAST ? __fdividef(1.0f, x) : 1.0f / x; }
+  static __device__ __forceinline__ float rcp(float x) { return FAST ? mufu_rcp(x) : 1.0f / x; }
 };
 
 // Compile-time cell traits.  NGP = gate rows per hidden unit in the tensor-core

@@ -48,7 +48,7 @@ eng.backward(a.variant, R, b, st, ga, dsf)
 torch.cuda.synchronize()
 
 
-def profile(name, grid, run, labels):
+def profile(name, grid, run, labels, extra=()):
     buf = torch.zeros(grid * a.seq * 8, dtype=torch.int64, device=dev)
     L.frnn_debug_profile(buf.data_ptr(), a.seq)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -73,10 +73,14 @@ def profile(name, grid, run, labels):
     for lab, vals in zip(labels, per):
         q = sorted(vals)
         print(f"   {lab:>26s}: {S.median(vals):8.0f} {q[len(q) // 10]:8.0f} {q[9 * len(q) // 10]:8.0f}   (median p10 p90)")
+    for lab, k0, k1 in extra:  # stamp k1 - stamp k0 of the same step (thread 0)
+        q = sorted(v[c][t][k1] - v[c][t][k0] for c in range(grid) for t in range(lo, hi))
+        print(f"   {lab:>26s}: {q[len(q) // 2]:8.0f} {q[len(q) // 10]:8.0f} {q[9 * len(q) // 10]:8.0f}   (median p10 p90)")
 
 
 profile("fwd", pf["grid"], lambda: eng.forward(a.variant, R, b, x, s0, st, ga),
         ["wait h + MMA issue", "trace(t-1)+x prefetch+MMA", "tmem->xs+pointwise", "publish(multicast)",
-         "loop"])
+         "loop"],
+        [("  of which tmem->xs+sync", 2, 5), ("  of which cell math", 5, 6), ("  of which h slice+sync", 6, 3)])
 profile("bwd", pb["grid"], lambda: eng.backward(a.variant, R, b, st, ga, dsf),
         ["absorb(wait+load+sum)", "jacobian", "mma", "partials out+arrive", "dx stores"])
