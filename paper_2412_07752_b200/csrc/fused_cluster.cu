@@ -246,19 +246,22 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
     mbar_wait(&bars[0], t & 1);
     tc_fence_after();
     FRNN_PROF(2, t);
-    if (w < 4) {  // accumulators -> xs[b][row]
+    // accumulators -> xs[b][row]: warps 0-3 drain the M=128 block, warps 4-7 (same
+    // lane quadrants) the M=64 block in parallel
+    if (w < 4) {
       float v[16];
       tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc1, v);
       if (32 * w + l < a.R1) {
 #pragma unroll
         for (int n = 0; n < N; ++n) xs[n * XP + xs_row(32 * w + l)] = v[n];
       }
-      if (a.R2) {  // M=64 layout: rows 16w..16w+15 in lanes 32w..32w+15
-        tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc2, v);
-        if (l < 16 && 16 * w + l < a.R2) {
+    } else if (w < 8 && a.R2) {  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
+      const int q = w & 3;
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + a.acc2, v);
+      if (l < 16 && 16 * q + l < a.R2) {
 #pragma unroll
-          for (int n = 0; n < N; ++n) xs[n * XP + xs_row(a.R1 + 16 * w + l)] = v[n];
-        }
+        for (int n = 0; n < N; ++n) xs[n * XP + xs_row(a.R1 + 16 * q + l)] = v[n];
       }
     }
     tc_fence_before();
