@@ -363,6 +363,22 @@ def run_ours(a, rank, world, local_rank):
                                     "backward": 1e3 * ms3[1] / max(1, cnt3[1]) / a.seq},
             "kernel_ms_per_step": {"forward": ms3[0] / a.steps, "backward": ms3[1] / a.steps,
                                    "param_grads": ms3[2] / a.steps}}
+    if plan["forward"]["algo"] == 1 and dom < 2:
+        # fused kernels: R stays on-chip but the tensor core re-reads each CTA's
+        # slice as the A operand every step (TMEM for the M=128 block, SMEM for
+        # the rest).  At N=16 the MMA rate is set by that operand stream, not by
+        # FLOPs: tests/cuda/mma_bwd_bench.cu measures the forward mix at 294,912 B
+        # of A in 2,704 cycles on one SM (1.965 GHz) = 214 GB/s per SM.
+        ngp = {"elman": 1, "lstm": 4, "gru": 4, "slstm": 4}[a.variant]
+        dh = a.hidden // a.heads
+        a_bytes = 2.0 * a.heads * ngp * dh * dh  # gate rows padded to NGP, as tiled
+        sms = plan["backward" if dom == 1 else "forward"]["grid"]
+        gbs = a_bytes * a.seq / (avg_ms / 1e3) / 1e9
+        pk = 214.0 * sms
+        roof["operand_stream"] = {"bound": "tensor-core A operand (TMEM/SMEM)", "achieved": gbs, "peak": pk,
+                                  "unit": "GB/s", "frac": gbs / pk, "bytes_per_launch": a_bytes * a.seq,
+                                  "sms": sms, "note": "per-SM peak 214 GB/s: measured N=16 TS+SS64 MMA mix "
+                                                      "(profiles/r01_mma_bwd_mix_microbench.txt)"}
     if plan["forward"]["algo"] == 2 and dom < 2:
         # alternating path: R (beyond on-chip capacity) is streamed
         # from L2/HBM every step; its byte rate against the measured HBM copy peak
