@@ -36,10 +36,27 @@ __global__ void __launch_bounds__(384, 1) bench(int mode, int gap, long long* ou
   tc_fence_after();
   const uint32_t t = tb;
   const bool per = mode & 1, seq = mode & 2, none = mode & 4, wdg = mode & 8, spin = mode & 16, fen = mode & 32,
-             drain = mode & 64;
+             drain = mode & 64, absorb = mode & 256;
   const int last = per ? 3 : 0;
   long long dts[ITERS], iss[ITERS];
+  __shared__ uint64_t rbar;
+  if (tid == 0) {
+    mbar_init(&rbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  float sink = 0.f;
   for (int it = 0; it < ITERS; ++it) {
+    if (absorb) {  // like the backward's absorb: local arrive, cluster-scope acquire wait, 16 float2 reads
+      if (tid == 0) mbar_arrive_expect_tx(&rbar, 0);
+      mbar_wait_cluster(&rbar, it & 1);
+      const float* rp = reinterpret_cast<const float*>(sm + 98304) + 2 * tid;
+      for (int q = 0; q < 16; ++q) {
+        const float2 v = *reinterpret_cast<const float2*>(rp + q * 768);
+        sink += v.x + v.y;
+      }
+      __syncthreads();
+    }
     if (gap) {  // idle tensor pipe between bursts, like the rest of a recurrence step
       const long long g0 = clock64();
       while (clock64() - g0 < gap) {
@@ -93,6 +110,7 @@ __global__ void __launch_bounds__(384, 1) bench(int mode, int gap, long long* ou
       if (acc == 12345.f) out[31] = 1;
     }
   }
+  if (sink == 12345.f) out[30] = 1;
   if (tid == 0) {
     for (int i = 1; i < ITERS; ++i)
       for (int j = i; j > 0 && iss[j] < iss[j - 1]; --j) {
@@ -123,7 +141,7 @@ int main() {
   cudaFuncSetAttribute(bench, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* names[] = {"interleaved, 1 commit", "interleaved, per-pair commits", "sequential, 1 commit",
                          "sequential, per-pair commits", "no MMAs, 1 commit", "no MMAs, 4 commits"};
-  const int modes[] = {1, 5, 1 | 128, 5 | 128, 5 | 16 | 128, 1 | 8 | 16 | 32 | 64 | 128};
+  const int modes[] = {1, 1 | 256, 5 | 256, 1 | 8 | 16 | 32 | 64 | 128 | 256, 5 | 8 | 16 | 32 | 64 | 128 | 256};
   for (int cl : {16})
     for (int gap : {0})
     for (int mode : modes) {
