@@ -136,6 +136,14 @@ FRNN_API int frnn_workspace_size(const frnn_cell* cell, frnn_shape shape, int32_
  * planner.cpp:428-453): shape, kernel family, tiling, footprint, solve time. */
 FRNN_API int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
                             const frnn_options* opts, char* out, size_t out_bytes);
+/* Persistent plan cache (the paper's cached solver solutions):
+ * JSON lines, one solved plan per line (schema_version 1), tagged with the
+ * library version and device limits; load skips lines from another build or
+ * device.  Setting FRNN_PLAN_CACHE=<file> loads it before the first plan and
+ * appends every new solve. */
+FRNN_API int frnn_plan_cache_save(const char* path);
+FRNN_API int frnn_plan_cache_load(const char* path, int32_t* loaded);
+FRNN_API int frnn_plan_cache_clear(void);
 
 /* -- the hot path --------------------------------------------------------- */
 /* engine.hpp:143-203.  Writes states (incl. states[0] = s0) and gates. */

@@ -66,7 +66,8 @@ class Shard(C.Structure):
 
 EXPORTS = ["frnn_version", "frnn_last_error", "frnn_cell_spec", "frnn_plan", "frnn_workspace_size",
            "frnn_forward", "frnn_backward", "frnn_partition", "frnn_csp_solve", "frnn_csp_brute_force",
-           "frnn_input_projection", "frnn_plan_json"]
+           "frnn_input_projection", "frnn_plan_json", "frnn_plan_cache_save", "frnn_plan_cache_load",
+           "frnn_plan_cache_clear"]
 
 
 def lib_path() -> str:
@@ -242,6 +243,34 @@ def plan(variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto") -> d
     _check(load().frnn_plan(C.byref(cell_spec(variant)), Shape(T, B, NH, DH), DTYPE[dtype], PASS[pass_],
                             C.byref(o), C.byref(info)))
     return info.as_dict()
+
+
+def version() -> str:
+    """frnn_version(), without a device."""
+    L = load()
+    L.frnn_version.restype = C.c_char_p
+    return L.frnn_version().decode()
+
+
+def plan_cache_save(path) -> None:
+    """frnn_plan_cache_save: every plan solved so far, as JSON lines (schema_version 1)."""
+    L = load()
+    L.frnn_plan_cache_save.argtypes = [C.c_char_p]
+    _check(L.frnn_plan_cache_save(os.fsencode(path)))
+
+
+def plan_cache_load(path) -> int:
+    """frnn_plan_cache_load: merge a saved cache; returns the number of plans taken
+    (lines from another library version or device are skipped)."""
+    L = load()
+    L.frnn_plan_cache_load.argtypes = [C.c_char_p, C.POINTER(C.c_int32)]
+    n = C.c_int32(0)
+    _check(L.frnn_plan_cache_load(os.fsencode(path), C.byref(n)))
+    return n.value
+
+
+def plan_cache_clear() -> None:
+    _check(load().frnn_plan_cache_clear())
 
 
 def plan_json(variant, T, B, NH, DH, dtype="bf16", pass_="forward", algo="auto") -> dict:

@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -114,9 +115,137 @@ using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int, in
 std::mutex g_mu;
 std::map<Key, frnn::Plan> g_cache;
 
-int get_plan(const frnn::Problem& p, int pass, const frnn_options* o, frnn::Plan* out) {
+// ---------------------------------------------- persistent plan cache ----
+// The counterpart of the paper's cached solver solutions: solved
+// plans as JSON lines (schema_version 1, like frnn_plan_json), one per line,
+// keyed by the problem and the requested algorithm, tagged with the library
+// version and the device limits they were solved against.  Lines that do not
+// match this build and device are skipped on load.  FRNN_PLAN_CACHE=<file>
+// loads the file before the first plan and appends every new solve to it.
+int current_device() {
   int dev = 0;
-  cudaGetDevice(&dev);
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  return dev;
+}
+
+std::string plan_line(const Key& k, const frnn::Plan& pl) {
+  const auto& lim = frnn::device_limits();
+  char buf[1024];
+  std::snprintf(
+      buf, sizeof buf,
+      "{\"schema_version\": 1, \"version\": \"%s\", \"sm_count\": %d, \"smem_optin\": %d, "
+      "\"tmem_cols\": %d, \"cluster_max\": %d, \"variant\": %d, \"rec_mask\": %d, \"inp_mask\": %d, "
+      "\"seq_len\": %d, \"batch\": %d, \"num_heads\": %d, \"head_dim\": %d, \"bf16\": %d, \"pass\": %d, "
+      "\"req_algo\": %d, \"algo\": %d, \"rows_per_cta\": %d, \"batch_tile\": %d, \"units_per_cta\": %d, "
+      "\"ctas_per_group\": %d, \"groups\": %d, \"grid\": %d, \"threads\": %d, \"smem_bytes\": %d, "
+      "\"plan_tmem_cols\": %d, \"k_split\": %d, \"cluster\": %d, \"ka\": %d, \"stages\": %d, "
+      "\"ffma\": %d, \"ws_bytes\": %lld, \"solve_us\": %.3f}",
+      frnn_version(), lim.sm_count, lim.smem_optin, lim.tmem_cols, lim.cluster_max, std::get<0>(k), std::get<1>(k),
+      std::get<2>(k), std::get<3>(k), std::get<4>(k), std::get<5>(k), std::get<6>(k), std::get<7>(k),
+      std::get<8>(k), std::get<9>(k), pl.algo, pl.rows_per_cta, pl.batch_tile, pl.units_per_cta, pl.ctas_per_group,
+      pl.groups, pl.grid, pl.threads, pl.smem_bytes, pl.tmem_cols, pl.k_split, pl.cluster, pl.ka, pl.stages, pl.ffma,
+      (long long)pl.ws_bytes, pl.solve_us);
+  return buf;
+}
+
+bool field(const std::string& line, const char* name, double* v) {
+  const std::string pat = std::string("\"") + name + "\": ";
+  const size_t pos = line.find(pat);
+  if (pos == std::string::npos) return false;
+  char* end = nullptr;
+  *v = std::strtod(line.c_str() + pos + pat.size(), &end);
+  return end != line.c_str() + pos + pat.size();
+}
+
+// Parses one cache line; false when malformed or solved for another build/device.
+bool parse_plan_line(const std::string& line, int dev, Key* k, frnn::Plan* pl) {
+  const auto& lim = frnn::device_limits();
+  if (line.find(std::string("\"version\": \"") + frnn_version() + "\"") == std::string::npos) return false;
+  static const char* names[] = {"schema_version", "sm_count", "smem_optin", "tmem_cols", "cluster_max",
+                                "variant", "rec_mask", "inp_mask", "seq_len", "batch", "num_heads", "head_dim",
+                                "bf16", "pass", "req_algo", "algo", "rows_per_cta", "batch_tile",
+                                "units_per_cta", "ctas_per_group", "groups", "grid", "threads", "smem_bytes",
+                                "plan_tmem_cols", "k_split", "cluster", "ka", "stages", "ffma", "ws_bytes",
+                                "solve_us"};
+  double v[32];
+  for (int i = 0; i < 32; ++i)
+    if (!field(line, names[i], &v[i])) return false;
+  if (v[0] != 1 || v[1] != lim.sm_count || v[2] != lim.smem_optin || v[3] != lim.tmem_cols ||
+      v[4] != lim.cluster_max)
+    return false;
+  *k = Key{(int)v[5], (int)v[6], (int)v[7], (int)v[8], (int)v[9], (int)v[10], (int)v[11], (int)v[12],
+           (int)v[13], (int)v[14], dev, 0};
+  *pl = frnn::Plan{};
+  pl->algo = (int)v[15];
+  pl->rows_per_cta = (int)v[16];
+  pl->batch_tile = (int)v[17];
+  pl->units_per_cta = (int)v[18];
+  pl->ctas_per_group = (int)v[19];
+  pl->groups = (int)v[20];
+  pl->grid = (int)v[21];
+  pl->threads = (int)v[22];
+  pl->smem_bytes = (int)v[23];
+  pl->tmem_cols = (int)v[24];
+  pl->k_split = (int)v[25];
+  pl->cluster = (int)v[26];
+  pl->ka = (int)v[27];
+  pl->stages = (int)v[28];
+  pl->ffma = (int)v[29];
+  pl->ws_bytes = (size_t)v[30];
+  pl->solve_us = v[31];
+  return true;
+}
+
+int load_plans(const char* path, int* loaded) {  // caller holds g_mu
+  std::FILE* f = std::fopen(path, "r");
+  if (!f) return fail(FRNN_EINVAL_ARG, std::string("cannot open plan cache ") + path);
+  const int dev = current_device();
+  int n = 0;
+  std::string line;
+  char chunk[512];
+  while (std::fgets(chunk, sizeof chunk, f)) {
+    line += chunk;
+    if (line.empty() || line.back() != '\n') continue;
+    Key k;
+    frnn::Plan pl;
+    if (parse_plan_line(line, dev, &k, &pl)) {
+      g_cache[k] = pl;
+      ++n;
+    }
+    line.clear();
+  }
+  Key k;
+  frnn::Plan pl;
+  if (!line.empty() && parse_plan_line(line, dev, &k, &pl)) {
+    g_cache[k] = pl;
+    ++n;
+  }
+  std::fclose(f);
+  if (loaded) *loaded = n;
+  return FRNN_OK;
+}
+
+const char* env_cache() {
+  const char* e = std::getenv("FRNN_PLAN_CACHE");
+  return e && *e ? e : nullptr;
+}
+
+int get_plan(const frnn::Problem& p, int pass, const frnn_options* o, frnn::Plan* out) {
+  static std::once_flag env_once;
+  std::call_once(env_once, [] {
+    if (const char* path = env_cache()) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (std::FILE* f = std::fopen(path, "r")) {  // a missing file is created on the first solve
+        std::fclose(f);
+        load_plans(path, nullptr);
+        g_err.clear();
+      }
+    }
+  });
+  const int dev = current_device();
   int recm = 0, inm = 0;
   for (int j = 0; j < 4; ++j) {
     recm |= p.rec[j] << j;
@@ -139,6 +268,12 @@ int get_plan(const frnn::Problem& p, int pass, const frnn_options* o, frnn::Plan
   if (rc != FRNN_OK) return fail(rc, why);
   std::lock_guard<std::mutex> lk(g_mu);
   g_cache[k] = *out;
+  if (const char* path = env_cache()) {  // persist the new solve
+    if (std::FILE* f = std::fopen(path, "a")) {
+      std::fprintf(f, "%s\n", plan_line(k, *out).c_str());
+      std::fclose(f);
+    }
+  }
   return FRNN_OK;
 }
 
@@ -181,6 +316,34 @@ int frnn_plan(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pa
   out->cluster = pl.cluster;
   out->workspace_bytes = (int64_t)pl.ws_bytes;
   out->solve_us = pl.solve_us;
+  return FRNN_OK;
+}
+
+int frnn_plan_cache_save(const char* path) {
+  g_err.clear();
+  if (!path) return fail(FRNN_EINVAL_ARG, "null path");
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::FILE* f = std::fopen(path, "w");
+  if (!f) return fail(FRNN_EINVAL_ARG, std::string("cannot write plan cache ") + path);
+  for (const auto& kv : g_cache) std::fprintf(f, "%s\n", plan_line(kv.first, kv.second).c_str());
+  std::fclose(f);
+  return FRNN_OK;
+}
+
+int frnn_plan_cache_load(const char* path, int32_t* loaded) {
+  g_err.clear();
+  if (!path) return fail(FRNN_EINVAL_ARG, "null path");
+  std::lock_guard<std::mutex> lk(g_mu);
+  int n = 0;
+  const int rc = load_plans(path, &n);
+  if (loaded) *loaded = n;
+  return rc;
+}
+
+int frnn_plan_cache_clear(void) {
+  g_err.clear();
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_cache.clear();
   return FRNN_OK;
 }
 

@@ -155,3 +155,53 @@ def test_plan_json_schema():
     for v, dh in (("lstm", 20), ("gru", 36), ("elman", 1000)):
         f = plan_json(v, 16, 8, 1, dh, "bf16", "forward")
         assert f["algo"] == "alternating" and f["tiling"]["step_kernels"] == "ffma"
+
+
+# ------------------------------------------- persistent plan cache ----
+CACHE_SHAPES = [("slstm", 1024, 16, 1, 768, "bf16", "forward"), ("slstm", 1024, 16, 1, 768, "bf16", "backward"),
+                ("lstm", 64, 8, 1, 64, "f32", "forward"), ("slstm", 1024, 64, 1, 3072, "bf16", "backward")]
+
+
+def test_plan_cache_roundtrip(tmp_path):
+    """Solved plans saved as JSON lines reload bit-identically without re-solving
+    (the reloaded solve_us is the saved one), and foreign lines are skipped."""
+    import json
+    from paper_2412_07752_b200 import abi
+    abi.plan_cache_clear()
+    before = [abi.plan(*s) for s in CACHE_SHAPES]
+    path = tmp_path / "plans.jsonl"
+    abi.plan_cache_save(path)
+    lines = path.read_text().splitlines()
+    assert len(lines) == len(CACHE_SHAPES)
+    for ln in lines:
+        j = json.loads(ln)
+        assert j["schema_version"] == 1 and j["version"] == abi.version() and j["sm_count"] > 0
+    # a line from another build, a truncated line and noise are ignored
+    other = json.loads(lines[0])
+    other["version"] = "flashrnn-b200 0.0.0 (other build)"
+    other["batch"] = 999
+    path.write_text("\n".join(lines + [json.dumps(other), lines[1][:40], "not json"]) + "\n")
+    abi.plan_cache_clear()
+    assert abi.plan_cache_load(path) == len(CACHE_SHAPES)
+    after = [abi.plan(*s) for s in CACHE_SHAPES]
+    assert after == before  # including solve_us: served from the cache, not re-solved
+    with pytest.raises(abi.FrnnError):
+        abi.plan_cache_load(tmp_path / "missing.jsonl")
+
+
+def test_plan_cache_env_persists_across_processes(tmp_path):
+    """FRNN_PLAN_CACHE=<file>: the first process solves and appends, the second
+    starts from the file and reports the first one's solve time."""
+    import json
+    import os
+    import subprocess
+    import sys
+    path = tmp_path / "env_plans.jsonl"
+    code = ("import json, sys; sys.path.insert(0, %r); from paper_2412_07752_b200 import abi; "
+            "print(json.dumps(abi.plan('slstm', 1024, 16, 1, 768, 'bf16', 'backward')))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, FRNN_PLAN_CACHE=str(path))
+    runs = [json.loads(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                                      check=True).stdout.strip().splitlines()[-1]) for _ in range(2)]
+    assert runs[0] == runs[1]
+    assert len(path.read_text().splitlines()) == 1  # the second process did not solve again
