@@ -631,10 +631,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         for (int mb = 0; mb < MB; ++mb) {
           if (a.skeleton) {
           } else if (mb < MBT) {
-            mma_chain_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
+            mma_run_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
           } else {
-            mma_chain_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)),
-                         (2 * 128 * 16) >> 4, bd, (2 * LBO) >> 4, idesc, nk);
+            mma_run_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)),
+                       (2 * 128 * 16) >> 4, bd, (2 * LBO) >> 4, idesc, nk);
           }
           if (elect_one()) mma_commit(&blkbar[mb]);
           __syncwarp();

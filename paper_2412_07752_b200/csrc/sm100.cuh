@@ -160,6 +160,81 @@ __device__ __forceinline__ void mma_chain_ts_ss(uint32_t d1, uint32_t a1, uint32
       : "memory");
 }
 
+// Straight-line MMA runs: the step loop of the chains above costs ~15 SASS
+// instructions per MMA (loop counter, vector-predicate branch, re-election),
+// which at N=16 is longer than the MMA itself when the issuing warp shares its
+// scheduler with busy warps.  These issue 4 steps per asm block (one
+// elect.sync, then add + mma per step), and the C++ wrappers below cover any
+// step count with 4-step blocks plus single steps.  accumulate = (k > 0 || acc).
+#define FRNN_MMA_HEAD(ACC)                                  \
+  ".reg .pred e, p, t;\n\t"                                  \
+  "elect.sync _|e, 0xffffffff;\n\t"                          \
+  "setp.ne.b32 p, " ACC ", 0;\n\tsetp.eq.b32 t, " ACC ", " ACC ";\n\t"
+// operands: %0 d, %1 A (tmem address), %2 B desc, %3 B step, %4 idesc, %5 acc
+__device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t ta, uint64_t bd, uint64_t bk, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%5")
+      ".reg .b32 a;\n\t.reg .b64 b;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, p;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t}" ::"r"(d),
+      "r"(ta), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// operands: %0 d, %1 A (tmem address), %2 B desc, %3 idesc, %4 acc
+__device__ __forceinline__ void mma1_ts(uint32_t d, uint32_t ta, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%4")
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(ta), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// operands: %0 d, %1 A desc, %2 A step, %3 B desc, %4 B step, %5 idesc, %6 acc
+__device__ __forceinline__ void mma4_ss(uint32_t d, uint64_t ad, uint64_t ak, uint64_t bd, uint64_t bk,
+                                        uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%6")
+      ".reg .b64 a, b;\n\tmov.b64 a, %1;\n\tmov.b64 b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, p;\n\t"
+      "add.u64 a, a, %2;\n\tadd.u64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t"
+      "add.u64 a, a, %2;\n\tadd.u64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t"
+      "add.u64 a, a, %2;\n\tadd.u64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %5, t;\n\t}" ::"r"(d),
+      "l"(ad), "l"(ak), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// operands: %0 d, %1 A desc, %2 B desc, %3 idesc, %4 acc
+__device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%4")
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// Whole warp.  D[d] (+)= sum_k A(a0 + k*a_step) . B(b0 + k*b_step), k < n.
+__device__ __forceinline__ void mma_run_ts(uint32_t d, uint32_t a0, uint32_t a_step, uint64_t b0, uint64_t b_step,
+                                           uint32_t idesc, int n) {
+  int k = 0;
+  if (a_step == 8) {
+    for (; k + 4 <= n; k += 4) mma4_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0);
+  }
+  for (; k < n; ++k) mma1_ts(d, a0 + a_step * k, b0 + (uint64_t)k * b_step, idesc, k > 0);
+}
+__device__ __forceinline__ void mma_run_ss(uint32_t d, uint64_t a0, uint64_t a_step, uint64_t b0, uint64_t b_step,
+                                           uint32_t idesc, int n) {
+  int k = 0;
+  for (; k + 4 <= n; k += 4)
+    mma4_ss(d, a0 + (uint64_t)k * a_step, a_step, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0);
+  for (; k < n; ++k) mma1_ss(d, a0 + (uint64_t)k * a_step, b0 + (uint64_t)k * b_step, idesc, k > 0);
+}
+
 // K-outer / block-inner issue over several independent accumulators, so that
 // consecutive MMAs never target the same D (no accumulate-dependency stalls):
 //   for k < nk:  for i < nts: D[d0 + i*dstep] (+)= A_tmem[ta0 + i*tblk + 8k] . B(k)
