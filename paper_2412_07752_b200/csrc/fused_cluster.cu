@@ -217,10 +217,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       const uint64_t bd = sdesc_kmajor(smem_u32(buf ? hB1 : hB0), LBO, SBO);
       if (a.skeleton) {
       } else if (a.R2) {
-        mma_chain_ts_ss(tbase + a.acc1, tbase, 8, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
-                        (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, K / 16);
+        mma_run_ts_ss(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
+                      (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, K / 16);
       } else {
-        mma_chain_ts(tbase + a.acc1, tbase, 8, bd, (2 * LBO) >> 4, idesc1, K / 16);
+        mma_run_ts(tbase + a.acc1, tbase, 8, bd, (2 * LBO) >> 4, idesc1, K / 16);
       }
       if (elect_one()) mma_commit(&bars[0]);
       __syncwarp();

@@ -218,6 +218,45 @@ __device__ __forceinline__ void mma1_ss(uint32_t d, uint64_t ad, uint64_t bd, ui
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
       : "memory");
 }
+// Interleaved TS (M=128, into d1) + SS (into d2) pairs sharing B, 4 steps.
+// operands: %0 d1, %1 A1 tmem, %2 d2, %3 A2 desc, %4 A2 step, %5 B desc, %6 B step, %7 idesc1, %8 idesc2, %9 acc
+__device__ __forceinline__ void mma4_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t ad, uint64_t ak,
+                                           uint64_t bd, uint64_t bk, uint32_t id1, uint32_t id2, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%9")
+      ".reg .b32 x;\n\t.reg .b64 a, b;\n\tmov.b32 x, %1;\n\tmov.b64 a, %3;\n\tmov.b64 b, %5;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, p;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t}" ::"r"(d1),
+      "r"(ta), "r"(d2), "l"(ad), "l"(ak), "l"(bd), "l"(bk), "r"(id1), "r"(id2), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma1_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t ad, uint64_t bd,
+                                           uint32_t id1, uint32_t id2, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%7")
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], %3, %4, %6, p;\n\t}" ::"r"(d1),
+      "r"(ta), "r"(d2), "l"(ad), "l"(bd), "r"(id1), "r"(id2), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t d2, uint64_t a2, uint64_t a2_step,
+                                              uint64_t b0, uint64_t b_step, uint32_t id1, uint32_t id2, int n) {
+  int k = 0;
+  for (; k + 4 <= n; k += 4)
+    mma4_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, a2_step, b0 + (uint64_t)k * b_step, b_step, id1,
+               id2, k > 0);
+  for (; k < n; ++k)
+    mma1_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, b0 + (uint64_t)k * b_step, id1, id2, k > 0);
+}
 // Whole warp.  D[d] (+)= sum_k A(a0 + k*a_step) . B(b0 + k*b_step), k < n.
 __device__ __forceinline__ void mma_run_ts(uint32_t d, uint32_t a0, uint32_t a_step, uint64_t b0, uint64_t b_step,
                                            uint32_t idesc, int n) {
