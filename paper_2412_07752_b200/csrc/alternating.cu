@@ -210,11 +210,7 @@ __global__ void __launch_bounds__(ATHREADS, 1)
       if (!(a.dbg & 4)) {
         for (int q = 0; q < a.ka; ++q) {
           const uint64_t ad = sdesc_k_sw128(sa + q * A_BYTES), bd = sdesc_k_sw128(sa + a.a_bytes + q * N * 128);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (elect_one()) mma_ss(tbase, ad + 2 * k, bd + 2 * k, idesc, (kb | q | k) ? 1u : 0u);
-            __syncwarp();
-          }
+          mma4_ss(tbase, ad, 2, bd, 2, idesc, (kb | q) ? 1u : 0u);  // the atom's 4 K=16 steps
         }
       }
       if (elect_one()) {
@@ -390,11 +386,7 @@ __global__ void __launch_bounds__(ATHREADS, 1)
         for (int q = 0; q < a.ka; ++q) {
           const uint64_t ad = sdesc_mn_sw128_chunk(sa + q * A_BYTES, A_BYTES / 2),
                          bd = sdesc_k_sw128(sa + a.a_bytes + q * N * 128);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (elect_one()) mma_ss(tbase, ad + 128 * k, bd + 2 * k, idesc, (i | q | k) ? 1u : 0u);
-            __syncwarp();
-          }
+          mma4_ss(tbase, ad, 128, bd, 2, idesc, (i | q) ? 1u : 0u);
         }
         if (elect_one()) mma_commit(&s.empty[st]);
         __syncwarp();
