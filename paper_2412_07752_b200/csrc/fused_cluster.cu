@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + nbuf) * a.CL + me) * a.slice;
       for (int i = tid; i < (int)(a.slice / 16); i += NT)
         reinterpret_cast<uint4*>(gst)[i] = reinterpret_cast<const uint4*>(hs)[i];
-      fence_proxy_async_global();
+      if (tid < (int)(a.slice / 16)) fence_proxy_async_global();  // the writers' generic -> async proxy order
       __syncthreads();
       FRNN_PROF(7, t);
       if (tid == 0) {
