@@ -29,6 +29,7 @@
 // MMAs are issued by warp 0 as whole-warp PTX loops (sm100.cuh mma_chain_*).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "cells.cuh"
@@ -55,6 +56,7 @@ struct CArgs {
   int K;           // forward contraction = DH (multiple of 16)
   int KBP;         // backward contraction = UPC*NGP padded to 16
   int MB, MBT;     // backward: 128-column blocks of DH / how many have A in TMEM
+  int MS, SSM;     // backward: SMEM-A column blocks of SSM (64 | 128) columns
   uint32_t tmem_cols, acc1, acc2;
   uint32_t slice;  // forward: bytes of one CTA's h slice
   bf16* xstage;    // forward staging [groups][2][CL][slice]
@@ -371,20 +373,21 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   bf16* dx = static_cast<bf16*>(p.dx);
   bf16* ds0 = static_cast<bf16*>(p.ds0);
   const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * 4;
-  const size_t blk_bytes = (size_t)128 * KBP * 2;
+  const int MS = a.MS, SSM = a.SSM, NPAIR = max(MBT, MS);
+  const size_t blk_bytes = (size_t)SSM * KBP * 2;  // one SMEM-A block
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const bool dsm = a.dsm != 0;
   const int TP = a.UPC + 2;                                              // term pitch (bank spread)
-  uint8_t* AS = smem;                                                    // (MB-MBT) x [128 x KBP] K-major
-  float* recv = reinterpret_cast<float*>(AS + (MB - MBT) * blk_bytes);  // global mode: [CL src][N][UPC]
+  uint8_t* AS = smem;                                                    // MS x [SSM x KBP] K-major
+  float* recv = reinterpret_cast<float*>(AS + MS * blk_bytes);          // global mode: [CL src][N][UPC]
   float* recv1 = dsm ? recv + recv_bytes / 4 : recv;                    // DSMEM mode: 2 x [CL src][UPC][N]
   uint8_t* dgB = reinterpret_cast<uint8_t*>(recv1) + recv_bytes;        // [N x KBP] K-major
   float* dbs = reinterpret_cast<float*>(dgB + N * KBP * 2);             // [NG][N][UPC] db scratch
   float* term = dbs + NG * N * a.UPC;                                    // DSMEM mode: [N][TP] summed R^T dg
   uint64_t* bars = reinterpret_cast<uint64_t*>(term + (dsm ? N * TP : 0));  // -, rcv, rdy0|rcv0, rdy1|rcv1
-  uint64_t* blkbar = bars + 4;  // [MB]: MMA of column block mb (and all before it) complete
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(blkbar + 8);
+  uint64_t* blkbar = bars + 4;  // [NPAIR]: MMAs of block pair i (and all before it) complete
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(blkbar + 16);
 
   if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
   if (tid == 0) {
@@ -392,18 +395,18 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], dsm ? 1 : a.CL);
     mbar_init(&bars[3], dsm ? 1 : a.CL);
-    for (int i = 0; i < MB; ++i) mbar_init(&blkbar[i], 1);
+    for (int i = 0; i < NPAIR; ++i) mbar_init(&blkbar[i], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < N * KBP * 2 / 16; i += NT) reinterpret_cast<uint4*>(dgB)[i] = make_uint4(0, 0, 0, 0);
-  if (recur) {  // R_slice^T blocks in SMEM: element (column m, row k) of block mb
-    for (int mb = MBT; mb < MB; ++mb) {
-      uint8_t* blk = AS + (mb - MBT) * blk_bytes;
-      for (int i = tid; i < 128 * KBP; i += NT) {
-        const int m = i % 128, k = i / 128, c = mb * 128 + m, uu = k / NGP, g = k % NGP;
+  if (recur) {  // R_slice^T blocks in SMEM: element (column m, row k) of block ib
+    for (int ib = 0; ib < MS; ++ib) {
+      uint8_t* blk = AS + ib * blk_bytes;
+      for (int i = tid; i < SSM * KBP; i += NT) {
+        const int m = i % SSM, k = i / SSM, c = MBT * 128 + ib * SSM + m, uu = k / NGP, g = k % NGP;
         const float v = (c < DH && uu < a.UPC && g < NG && p.rec[g])
                             ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
-        *reinterpret_cast<bf16*>(blk + kmaj(m, k, 128)) = __float2bfloat16_rn(v);
+        *reinterpret_cast<bf16*>(blk + kmaj(m, k, SSM)) = __float2bfloat16_rn(v);
       }
     }
   }
@@ -622,21 +625,27 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       fence_proxy_async_smem();
       __syncthreads();
       FRNN_PROF(2, k);
-      if (w == 0) {  // column blocks in order (TMEM-A, then SMEM-A), one commit per block so
-                     // the drain + exchange of block mb overlaps the MMAs of the later blocks
+      if (w == 0) {  // block pairs in order: TMEM-A block i interleaved step by step with SMEM-A
+                     // block i (the two operand paths overlap), one commit per pair so the drain +
+                     // exchange of pair i overlaps the MMAs of the later pairs
         tc_fence_after();
         const uint64_t bd = sdesc_kmajor(smem_u32(dgB), LBO, SBO);
-        const uint64_t ad = sdesc_kmajor(smem_u32(AS), 128 * 16, 128);
+        const uint64_t ad = sdesc_kmajor(smem_u32(AS), SSM * 16, 128);
+        const uint32_t idesc2 = idesc_bf16(SSM, N);
         const int nk = KBP / 16, cb = KBP / 2;
-        for (int mb = 0; mb < MB; ++mb) {
+        for (int i = 0; i < NPAIR; ++i) {
+          const uint32_t accT = tbase + a.acc1 + i * N, accS = tbase + a.acc1 + (MBT + i) * N;
+          const uint64_t adS = ad + (uint64_t)(i * (blk_bytes >> 4));
           if (a.skeleton) {
-          } else if (mb < MBT) {
-            mma_run_ts(tbase + a.acc1 + mb * N, tbase + mb * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
+          } else if (i < MBT && i < MS) {
+            mma_run_ts_ss(accT, tbase + i * cb, accS, adS, (2 * SSM * 16) >> 4, bd, (2 * LBO) >> 4, idesc, idesc2,
+                          nk);
+          } else if (i < MBT) {
+            mma_run_ts(accT, tbase + i * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
           } else {
-            mma_run_ss(tbase + a.acc1 + mb * N, ad + (uint64_t)((mb - MBT) * (blk_bytes >> 4)),
-                       (2 * 128 * 16) >> 4, bd, (2 * LBO) >> 4, idesc, nk);
+            mma_run_ss(accS, adS, (2 * SSM * 16) >> 4, bd, (2 * LBO) >> 4, idesc2, nk);
           }
-          if (elect_one()) mma_commit(&blkbar[mb]);
+          if (elect_one()) mma_commit(&blkbar[i]);
           __syncwarp();
         }
       }
@@ -646,13 +655,33 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       float* base = a.pstage + (((size_t)grp * 2 + (t & 1)) * a.CL) * a.CL * N * a.UPC;
       const int qd = w & 3;
       const uint32_t rb = smem_u32((t & 1) ? recv1 : recv), rbar = smem_u32(&bars[2 + (t & 1)]);
-      for (int mb = w >> 2; mb < MB; mb += NT >> 7) {
-        mbar_wait(&blkbar[mb], mma_phase);
+      // the MBT + MS accumulator blocks (pair order: TMEM-A block i, then SMEM-A block i)
+      // are dealt round-robin to the NT/128 warp groups
+      const int both = min(MBT, MS), nent = MBT + MS, ngrp = NT >> 7;
+      for (int ent = w >> 2; ent < nent; ent += ngrp) {
+        int i, sblk;
+        if (ent < 2 * both) {
+          i = ent >> 1;
+          sblk = ent & 1;
+        } else {
+          i = both + (ent - 2 * both);
+          sblk = MS > MBT;
+        }
+        mbar_wait(&blkbar[i], mma_phase);
         tc_fence_after();
-        const int c = mb * 128 + 32 * qd + l;
+        int c;
+        bool lane_ok = true;
+        if (!sblk) {
+          c = i * 128 + 32 * qd + l;
+        } else if (SSM == 64) {  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
+          c = MBT * 128 + i * 64 + 16 * qd + l;
+          lane_ok = l < 16;
+        } else {
+          c = MBT * 128 + i * 128 + 32 * qd + l;
+        }
         float v[16];
-        tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + mb * N, v);
-        if (c < DH) {
+        tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (sblk ? MBT + i : i) * N, v);
+        if (lane_ok && c < DH) {
           const int q = c / a.UPC, cu = c % a.UPC;
           if (a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
                              // 32 consecutive columns = one contiguous 128-byte row segment per n
@@ -754,13 +783,24 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
              align_up(s.slice, 16) + 64;
     s.ws = align_up((size_t)s.groups * 2 * s.CL * s.slice, 256);
   } else {
+    // R_p^T column blocks: MBT of 128 columns with A in TMEM, then MS of SSM
+    // columns with A in SMEM, issued as pairs (TMEM block i interleaved with
+    // SMEM block i, the two operand paths overlap); accumulators (MBT + MS) x N.
+    // SSM = 128 measured best (sLSTM H=768 backward 4.42 us/step vs 4.84 with
+    // 64-column SMEM blocks and 4.75 with no interleaving).
     const int colblk = s.KBP / 2;
-    int mbt = (512 - s.MB * N) / colblk;
-    s.MBT = mbt < s.MB ? (mbt < 0 ? 0 : mbt) : s.MB;
+    const char* se = getenv("FRNN_BWD_SSM");  // A/B hook: 64 = SMEM blocks of 64 columns
+    s.SSM = se && atoi(se) == 64 ? 64 : 128;
+    auto ms_of = [&](int mbt) { return p.DH > 128 * mbt ? (p.DH - 128 * mbt + s.SSM - 1) / s.SSM : 0; };
+    int mbt = s.MB;
+    while (mbt > 0 && mbt * colblk + (mbt + ms_of(mbt)) * N > 512) --mbt;
+    s.MBT = mbt;
+    s.MS = ms_of(mbt);
+    if (std::max(s.MBT, s.MS) > 16) s.EPT = 0;  // 16 block-pair mbarriers
     s.acc1 = (uint32_t)(s.MBT * colblk);
-    s.tmem_cols = pow2_cols(s.acc1 + s.MB * N);
-    s.smem = (size_t)(s.MB - s.MBT) * 128 * s.KBP * 2 + (size_t)s.CL * N * UPC * 4 + (size_t)N * s.KBP * 2 +
-             (size_t)p.NG * N * UPC * 4 + 128;  // + 4 exchange and 8 block mbarriers, TMEM base
+    s.tmem_cols = pow2_cols(s.acc1 + (s.MBT + s.MS) * N);
+    s.smem = (size_t)s.MS * s.SSM * s.KBP * 2 + (size_t)s.CL * N * UPC * 4 + (size_t)N * s.KBP * 2 +
+             (size_t)p.NG * N * UPC * 4 + 192;  // + 4 exchange and 16 block-pair mbarriers, TMEM base
     // DSMEM exchange: a second (parity) receive buffer + the summed-term tile
     const size_t dsm_smem = s.smem + (size_t)s.CL * N * UPC * 4 + (size_t)N * (UPC + 2) * 4;
     const char* xe = getenv("FRNN_XCHG");  // A/B hook: 0 = global + TMA bulk load, 1 = DSMEM v4 [cu][n], 2 = rows
@@ -790,6 +830,8 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.KBP = cs.KBP;
   a.MB = cs.MB;
   a.MBT = cs.MBT;
+  a.MS = cs.MS;
+  a.SSM = cs.SSM;
   a.tmem_cols = cs.tmem_cols;
   a.acc1 = cs.acc1;
   a.acc2 = cs.acc2;

@@ -60,6 +60,7 @@ size_t fused_backward_ws(const Problem& p, const Plan& pl);
 constexpr int kSmemOptin = 232448;  // B200 max dynamic shared memory per CTA (opt-in)
 struct ClusterShape {
   int UPC, CL, R1, R2, K, KBP, MB, MBT, EPT, groups, threads;
+  int MS, SSM;  // backward: SMEM-A column blocks and their M (64 | 128)
   int dsm;  // backward partial exchange: 0 global + TMA bulk load, 1 DSMEM v4 [cu][n], 2 DSMEM rows [n][cu]
   uint32_t acc1, acc2, tmem_cols, slice;
   size_t smem, ws;

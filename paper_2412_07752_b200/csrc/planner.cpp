@@ -116,16 +116,19 @@ Builder cluster_csp(const Problem& p, int pass, const DeviceLimits& lim, int thr
     // TMEM: R slice as bf16 pairs (DH/2 columns, 32-aligned) + two N-wide accumulators
     b.le(b.k(((DH / 2 + 31) / 32) * 32 + 2 * N), lim.tmem_cols);
   } else {
-    // Backward: R_p^T as MB 128-column blocks (MBT in TMEM, the rest in SMEM),
-    // K = rows padded to 16 (KBH = K/2 TMEM columns per block)
+    // Backward: R_p^T as MBT 128-column blocks in TMEM and MS 128-column blocks
+    // in SMEM, K = rows padded to 16 (KBH = K/2 TMEM columns per block)
     auto MBT = b.var("MBT", Domain::span(1, MB));
+    auto MS1 = b.var("MS1", Domain::span(1, 17));  // MS + 1 (domains are positive)
     auto KBH = b.var("KBH", Domain::grid(8, 128, 8));
     b.le(UPC * NGP, KBH * 2);
     b.le(KBH * 2, UPC * NGP + 15);
-    b.le(MBT * KBH + MB * N, lim.tmem_cols);
-    // SMEM: (MB-MBT) blocks [128 x K] + partial receive [CL][N][UPC] fp32 + dg tile + db scratch
-    b.le(KBH * (MB * 512 + N * 4) + CL * UPC * (N * 4) + UPC * (p.NG * N * 4) + 128,
-         b.k(lim.smem_optin) + MBT * KBH * 512);
+    b.le(b.k(DH + 128), MBT * 128 + MS1 * 128);                 // the blocks cover DH columns
+    b.le(MBT + MS1, b.k(MB + 1));                               // MBT + MS = MB
+    b.le(MBT * KBH + (MBT + MS1) * N, b.k(lim.tmem_cols + N));  // A blocks + accumulators
+    // SMEM: MS blocks [128 x K] + partial receive [CL][N][UPC] fp32 + dg tile + db scratch
+    b.le(MS1 * KBH * 512 + KBH * (N * 4) + CL * UPC * (N * 4) + UPC * (p.NG * N * 4) + 192,
+         b.k(lim.smem_optin) + KBH * 512);
   }
   // Heuristic (planner.cpp:203-228 in spirit): fewest CTAs synchronising per
   // step, fewest batch tiles, fill TMEM before SMEM, most R^T in TMEM.
@@ -134,6 +137,7 @@ Builder cluster_csp(const Problem& p, int pass, const DeviceLimits& lim, int thr
   b.prefer("R1", Pref::Largest);
   if (pass == 1) {
     b.prefer("MBT", Pref::Largest);
+    b.prefer("MS1", Pref::Smallest);
     b.prefer("KBH", Pref::Smallest);
   }
   b.prefer("A2P1", Pref::Smallest);
