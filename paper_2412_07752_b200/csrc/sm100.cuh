@@ -249,22 +249,25 @@ __device__ __forceinline__ void mma1_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2
       : "memory");
 }
 __device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t d2, uint64_t a2, uint64_t a2_step,
-                                              uint64_t b0, uint64_t b_step, uint32_t id1, uint32_t id2, int n) {
+                                              uint64_t b0, uint64_t b_step, uint32_t id1, uint32_t id2, int n,
+                                              bool acc0 = false) {
   int k = 0;
   for (; k + 4 <= n; k += 4)
     mma4_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, a2_step, b0 + (uint64_t)k * b_step, b_step, id1,
-               id2, k > 0);
+               id2, k > 0 || acc0);
   for (; k < n; ++k)
-    mma1_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, b0 + (uint64_t)k * b_step, id1, id2, k > 0);
+    mma1_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, b0 + (uint64_t)k * b_step, id1, id2,
+               k > 0 || acc0);
 }
 // Whole warp.  D[d] (+)= sum_k A(a0 + k*a_step) . B(b0 + k*b_step), k < n.
+// acc0: accumulate onto D from the first step too (a K range continuing a sum).
 __device__ __forceinline__ void mma_run_ts(uint32_t d, uint32_t a0, uint32_t a_step, uint64_t b0, uint64_t b_step,
-                                           uint32_t idesc, int n) {
+                                           uint32_t idesc, int n, bool acc0 = false) {
   int k = 0;
   if (a_step == 8) {
-    for (; k + 4 <= n; k += 4) mma4_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0);
+    for (; k + 4 <= n; k += 4) mma4_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0 || acc0);
   }
-  for (; k < n; ++k) mma1_ts(d, a0 + a_step * k, b0 + (uint64_t)k * b_step, idesc, k > 0);
+  for (; k < n; ++k) mma1_ts(d, a0 + a_step * k, b0 + (uint64_t)k * b_step, idesc, k > 0 || acc0);
 }
 __device__ __forceinline__ void mma_run_ss(uint32_t d, uint64_t a0, uint64_t a_step, uint64_t b0, uint64_t b_step,
                                            uint32_t idesc, int n) {
