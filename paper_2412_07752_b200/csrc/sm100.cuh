@@ -186,6 +186,31 @@ __device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t ta, uint64_t bd, ui
       "r"(ta), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
       : "memory");
 }
+// 8 TS steps (operands as mma4_ts).
+__device__ __forceinline__ void mma8_ts(uint32_t d, uint32_t ta, uint64_t bd, uint64_t bk, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%5")
+      ".reg .b32 a;\n\t.reg .b64 b;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, p;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "}" ::"r"(d),
+      "r"(ta), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // operands: %0 d, %1 A (tmem address), %2 B desc, %3 idesc, %4 acc
 __device__ __forceinline__ void mma1_ts(uint32_t d, uint32_t ta, uint64_t bd, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -239,6 +264,39 @@ __device__ __forceinline__ void mma4_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2
       "r"(ta), "r"(d2), "l"(ad), "l"(ak), "l"(bd), "l"(bk), "r"(id1), "r"(id2), "r"(acc)
       : "memory");
 }
+// 8 steps of the interleaved pair (same operands as mma4_ts_ss).
+__device__ __forceinline__ void mma8_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t ad, uint64_t ak,
+                                           uint64_t bd, uint64_t bk, uint32_t id1, uint32_t id2, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%9")
+      ".reg .b32 x;\n\t.reg .b64 a, b;\n\tmov.b32 x, %1;\n\tmov.b64 a, %3;\n\tmov.b64 b, %5;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, p;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "}" ::"r"(d1),
+      "r"(ta), "r"(d2), "l"(ad), "l"(ak), "l"(bd), "l"(bk), "r"(id1), "r"(id2), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void mma1_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t ad, uint64_t bd,
                                            uint32_t id1, uint32_t id2, uint32_t acc) {
   asm volatile(
@@ -252,6 +310,9 @@ __device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t
                                               uint64_t b0, uint64_t b_step, uint32_t id1, uint32_t id2, int n,
                                               bool acc0 = false) {
   int k = 0;
+  for (; k + 8 <= n; k += 8)
+    mma8_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, a2_step, b0 + (uint64_t)k * b_step, b_step, id1,
+               id2, k > 0 || acc0);
   for (; k + 4 <= n; k += 4)
     mma4_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, a2_step, b0 + (uint64_t)k * b_step, b_step, id1,
                id2, k > 0 || acc0);
@@ -265,6 +326,7 @@ __device__ __forceinline__ void mma_run_ts(uint32_t d, uint32_t a0, uint32_t a_s
                                            uint32_t idesc, int n, bool acc0 = false) {
   int k = 0;
   if (a_step == 8) {
+    for (; k + 8 <= n; k += 8) mma8_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0 || acc0);
     for (; k + 4 <= n; k += 4) mma4_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0 || acc0);
   }
   for (; k < n; ++k) mma1_ts(d, a0 + a_step * k, b0 + (uint64_t)k * b_step, idesc, k > 0 || acc0);
