@@ -164,6 +164,25 @@ def test_bf16_fused_h768(eng, orc, v):
     check_bf16(eng, orc, v, inp)
 
 
+@pytest.mark.parametrize("v", ["slstm", "gru"])
+def test_bf16_cluster_three_batch_tiles(eng, orc, v):
+    """H=768 with B=40: three 16-row clusters per head (the last ragged) on the
+    cluster kernels' paired TMEM/SMEM column blocks."""
+    inp = orc.generate(v, 6, 40, 1, 768, seed=12)
+    assert eng.plan(v, 6, 40, 1, 768, "bf16", "backward")["cluster"] == 16
+    check_bf16(eng, orc, v, inp)
+
+
+@pytest.mark.parametrize("v,NH,DH,B", [("slstm", 1, 640, 24), ("slstm", 1, 896, 20), ("lstm", 2, 384, 24),
+                                       ("elman", 1, 512, 16)])
+def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
+    """Head dims whose tilings differ from the headline: DH=640 (UPC=40, five
+    TMEM blocks, no SMEM block), DH=896 (no cluster tiling: L2-flag fused
+    forward + alternating backward), two heads of 384, Elman 512."""
+    inp = orc.generate(v, 6, B, NH, DH, seed=13)
+    check_bf16(eng, orc, v, inp)
+
+
 @pytest.mark.parametrize("NH,DH", [(4, 192), (12, 64)])
 def test_bf16_lstm_heads(eng, orc, NH, DH):
     """Config 3: head-wise block-diagonal R."""
