@@ -638,10 +638,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           const uint64_t adS = ad + (uint64_t)(i * (blk_bytes >> 4));
           if (a.skeleton) {
           } else if (i < MBT && i < MS) {
-            mma_run_ts_ss(accT, tbase + i * cb, accS, adS, (2 * SSM * 16) >> 4, bd, (2 * LBO) >> 4, idesc, idesc2,
-                          nk);
+            if (nk == 12) mma12_ts_ss(accT, tbase + i * cb, accS, adS, (2 * SSM * 16) >> 4, bd, (2 * LBO) >> 4,
+                                      idesc, idesc2, 0);
+            else mma_run_ts_ss(accT, tbase + i * cb, accS, adS, (2 * SSM * 16) >> 4, bd, (2 * LBO) >> 4, idesc,
+                               idesc2, nk);
           } else if (i < MBT) {
-            mma_run_ts(accT, tbase + i * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
+            if (nk == 12) mma12_ts(accT, tbase + i * cb, bd, (2 * LBO) >> 4, idesc, 0);
+            else mma_run_ts(accT, tbase + i * cb, 8, bd, (2 * LBO) >> 4, idesc, nk);
           } else {
             mma_run_ss(accS, adS, (2 * SSM * 16) >> 4, bd, (2 * LBO) >> 4, idesc2, nk);
           }

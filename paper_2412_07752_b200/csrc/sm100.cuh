@@ -320,6 +320,83 @@ __device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t
     mma1_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, b0 + (uint64_t)k * b_step, id1, id2,
                k > 0 || acc0);
 }
+// 12-step blocks: a whole K=192 backward block (UPC=48, 4-gate cells) per asm.
+__device__ __forceinline__ void mma12_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t ad, uint64_t ak,
+                                            uint64_t bd, uint64_t bk, uint32_t id1, uint32_t id2, uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%9")
+      ".reg .b32 x;\n\t.reg .b64 a, b;\n\tmov.b32 x, %1;\n\tmov.b64 a, %3;\n\tmov.b64 b, %5;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, p;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "add.u32 x, x, 8;\n\tadd.u64 a, a, %4;\n\tadd.u64 b, b, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%2], a, b, %8, t;\n\t"
+      "}" ::"r"(d1),
+      "r"(ta), "r"(d2), "l"(ad), "l"(ak), "l"(bd), "l"(bk), "r"(id1), "r"(id2), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma12_ts(uint32_t d, uint32_t ta, uint64_t bd, uint64_t bk, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%5")
+      ".reg .b32 a;\n\t.reg .b64 b;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, p;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "}" ::"r"(d),
+      "r"(ta), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // Whole warp.  D[d] (+)= sum_k A(a0 + k*a_step) . B(b0 + k*b_step), k < n.
 // acc0: accumulate onto D from the first step too (a K range continuing a sum).
 __device__ __forceinline__ void mma_run_ts(uint32_t d, uint32_t a0, uint32_t a_step, uint64_t b0, uint64_t b_step,
