@@ -633,6 +633,22 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         const uint64_t ad = sdesc_kmajor(smem_u32(AS), SSM * 16, 128);
         const uint32_t idesc2 = idesc_bf16(SSM, N);
         const int nk = KBP / 16, cb = KBP / 2;
+        if (MBT == 4 && MS == 2 && nk == 12 && !a.skeleton) {  // the H=768, 4-gate layout, spelled out
+          const uint64_t a2k = (2 * SSM * 16) >> 4, bk = (2 * LBO) >> 4, bs = blk_bytes >> 4;
+          const uint32_t acc = tbase + a.acc1;
+          mma12_ts_ss(acc, tbase, acc + 4 * N, ad, a2k, bd, bk, idesc, idesc2, 0);
+          if (elect_one()) mma_commit(&blkbar[0]);
+          __syncwarp();
+          mma12_ts_ss(acc + N, tbase + cb, acc + 5 * N, ad + bs, a2k, bd, bk, idesc, idesc2, 0);
+          if (elect_one()) mma_commit(&blkbar[1]);
+          __syncwarp();
+          mma12_ts(acc + 2 * N, tbase + 2 * cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[2]);
+          __syncwarp();
+          mma12_ts(acc + 3 * N, tbase + 3 * cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[3]);
+          __syncwarp();
+        } else
         for (int i = 0; i < NPAIR; ++i) {
           const uint32_t accT = tbase + a.acc1 + i * N, accS = tbase + a.acc1 + (MBT + i) * N;
           const uint64_t adS = ad + (uint64_t)(i * (blk_bytes >> 4));
