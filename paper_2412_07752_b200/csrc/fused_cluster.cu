@@ -218,6 +218,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       tc_fence_after();
       const uint64_t bd = sdesc_kmajor(smem_u32(buf ? hB1 : hB0), LBO, SBO);
       if (a.skeleton) {
+      } else if (a.R2 && K == 768) {  // H=768 per head: 6 blocks of 8 K-steps, spelled out
+        const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 64 * 16, 128);
+        constexpr uint64_t a2k = (2 * 64 * 16) >> 4, bk = (2 * LBO) >> 4;
+        const uint32_t d1 = tbase + a.acc1, d2 = tbase + a.acc2;
+        mma8_ts_ss(d1, tbase, d2, a2, a2k, bd, bk, idesc1, idesc2, 0);
+        mma8_ts_ss(d1, tbase + 64, d2, a2 + 8 * a2k, a2k, bd + 8 * bk, bk, idesc1, idesc2, 1);
+        mma8_ts_ss(d1, tbase + 128, d2, a2 + 16 * a2k, a2k, bd + 16 * bk, bk, idesc1, idesc2, 1);
+        mma8_ts_ss(d1, tbase + 192, d2, a2 + 24 * a2k, a2k, bd + 24 * bk, bk, idesc1, idesc2, 1);
+        mma8_ts_ss(d1, tbase + 256, d2, a2 + 32 * a2k, a2k, bd + 32 * bk, bk, idesc1, idesc2, 1);
+        mma8_ts_ss(d1, tbase + 320, d2, a2 + 40 * a2k, a2k, bd + 40 * bk, bk, idesc1, idesc2, 1);
       } else if (a.R2) {
         mma_run_ts_ss(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
                       (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, K / 16);
