@@ -711,13 +711,20 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         float v[16];
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (sblk ? MBT + i : i) * N, v);
         if (lane_ok && c < DH) {
-          const int q = c / a.UPC, cu = c % a.UPC;
+          const bool u48 = a.UPC == 48;  // the H=768 tiling: constant divisor and stride
+          const int q = u48 ? c / 48 : c / a.UPC, cu = u48 ? c % 48 : c % a.UPC;
           if (a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
                              // 32 consecutive columns = one contiguous 128-byte row segment per n
-            const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * a.UPC + cu) * 4), q);
             const uint32_t mbr = mapa_shared(rbar, q);
+            if (u48) {
+              const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * 48 + cu) * 4), q);
 #pragma unroll
-            for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * a.UPC * 4), v[n], mbr);
+              for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * 48 * 4), v[n], mbr);
+            } else {
+              const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * a.UPC + cu) * 4), q);
+#pragma unroll
+              for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * a.UPC * 4), v[n], mbr);
+            }
           } else if (dsm) {  // push straight into the owner's recv[t&1][me][cu][:], completing bytes on its mbarrier
             const uint32_t dst = mapa_shared(rb + (uint32_t)(((me * a.UPC + cu) * N) * 4), q);
             const uint32_t mbr = mapa_shared(rbar, q);
