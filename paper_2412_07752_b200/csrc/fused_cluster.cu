@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         mma8_ts_ss(d1, tbase + 192, d2, a2 + 24 * a2k, a2k, bd + 24 * bk, bk, idesc1, idesc2, 1);
         mma8_ts_ss(d1, tbase + 256, d2, a2 + 32 * a2k, a2k, bd + 32 * bk, bk, idesc1, idesc2, 1);
         mma8_ts_ss(d1, tbase + 320, d2, a2 + 40 * a2k, a2k, bd + 40 * bk, bk, idesc1, idesc2, 1);
+      } else if (a.R2 && K == 192) {  // DH=192 per head (config 3): one 12-step block
+        mma12_ts_ss(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
+                    (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, 0);
       } else if (a.R2) {
         mma_run_ts_ss(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
                       (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, K / 16);
@@ -657,6 +660,14 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           __syncwarp();
           mma12_ts(acc + 3 * N, tbase + 3 * cb, bd, bk, idesc, 0);
           if (elect_one()) mma_commit(&blkbar[3]);
+          __syncwarp();
+        } else if (MBT == 2 && MS == 0 && nk == 12 && !a.skeleton) {  // DH=192 per head (config 3)
+          const uint64_t bk = (2 * LBO) >> 4;
+          mma12_ts(tbase + a.acc1, tbase, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[0]);
+          __syncwarp();
+          mma12_ts(tbase + a.acc1 + N, tbase + cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[1]);
           __syncwarp();
         } else
         for (int i = 0; i < NPAIR; ++i) {
