@@ -698,7 +698,26 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       // the MBT + MS accumulator blocks (pair order: TMEM-A block i, then SMEM-A block i)
       // are dealt round-robin to the NT/128 warp groups
       const int both = min(MBT, MS), nent = MBT + MS, ngrp = NT >> 7;
-      for (int ent = w >> 2; ent < nent; ent += ngrp) {
+      const bool fixed = MBT == 4 && MS == 2 && SSM == 128 && NT == 384 && a.UPC == 48 && a.dsm == 2 && DH == 768;
+      if (fixed) {  // the H=768 layout spelled out: warp group -> (pair, column base, accumulator block)
+        const int wg = w >> 2;
+        const int i0 = wg == 2 ? 1 : 0, c0 = wg == 0 ? 0 : wg == 1 ? 512 : 128, a0 = wg == 0 ? 0 : wg == 1 ? 4 : 1;
+        const int i1 = wg == 0 ? 1 : wg == 1 ? 2 : 3, c1 = wg == 0 ? 640 : wg == 1 ? 256 : 384,
+                  a1 = wg == 0 ? 5 : wg == 1 ? 2 : 3;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          mbar_wait(&blkbar[e ? i1 : i0], mma_phase);
+          tc_fence_after();
+          const int c = (e ? c1 : c0) + 32 * qd + l, q = c / 48, cu = c % 48;
+          float v[16];
+          tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (e ? a1 : a0) * N, v);
+          const uint32_t mbr = mapa_shared(rbar, q);
+          const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * 48 + cu) * 4), q);
+#pragma unroll
+          for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * 48 * 4), v[n], mbr);
+        }
+      }
+      for (int ent = fixed ? nent : w >> 2; ent < nent; ent += ngrp) {
         int i, sblk;
         if (ent < 2 * both) {
           i = ent >> 1;
