@@ -66,6 +66,7 @@ struct CArgs {
   long long* prof;
   int prof_steps;
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
+  int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
   int skeleton;    // 1: synchronisation skeleton only -- no MMAs, no cell math (the sequential-
                    //    dependency floor of SURVEY 8d; frnn_debug_skeleton, results are garbage)
 };
@@ -385,7 +386,8 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const bf16* dh = static_cast<const bf16*>(p.dh);
   bf16* dx = static_cast<bf16*>(p.dx);
   bf16* ds0 = static_cast<bf16*>(p.ds0);
-  const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * 4;
+  const bool pbf = a.pbf16 && a.dsm == 2;  // partials exchanged as bf16 pairs (n, n+1)
+  const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * (pbf ? 2 : 4);
   const int MS = a.MS, SSM = a.SSM, NPAIR = max(MBT, MS);
   const size_t blk_bytes = (size_t)SSM * KBP * 2;  // one SMEM-A block
 
@@ -528,7 +530,22 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
     mbar_wait_cluster(&bars[2 + pb], (par_phase >> pb) & 1u);
     par_phase ^= 1u << pb;
-    if (own) {
+    if (own && pbf) {  // words [src][n/2][cu]: the (u, u+1) pair of words, half b&1 of each
+      const uint32_t* rp = reinterpret_cast<const uint32_t*>(pb ? recv1 : recv) + (size_t)(b >> 1) * a.UPC + u;
+      const size_t qs = (size_t)(N / 2) * a.UPC;
+      float t0 = 0.f, t1 = 0.f;
+      for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
+        const uint2 v = *reinterpret_cast<const uint2*>(rp + q * qs);
+        t0 += (b & 1) ? hi16(v.x) : lo16(v.x);
+        t1 += (b & 1) ? hi16(v.y) : lo16(v.y);
+      }
+      if (p.clip_mode == 1) {
+        t0 = fminf(fmaxf(t0, -mag), mag);
+        t1 = fminf(fmaxf(t1, -mag), mag);
+      }
+      ds[0][0] += t0;
+      ds[0][1] += t1;
+    } else if (own) {
       const float* rp = (pb ? recv1 : recv) + (size_t)b * a.UPC + u;
       const size_t qs = (size_t)N * a.UPC;
       float t0 = 0.f, t1 = 0.f;
@@ -712,9 +729,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           float v[16];
           tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (e ? a1 : a0) * N, v);
           const uint32_t mbr = mapa_shared(rbar, q);
-          const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * 48 + cu) * 4), q);
+          if (pbf) {  // words [src][n/2][cu] = bf16 (n even, n odd)
+            const uint32_t dst = mapa_shared(rb + (uint32_t)((me * (N / 2) * 48 + cu) * 4), q);
 #pragma unroll
-          for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * 48 * 4), v[n], mbr);
+            for (int n2 = 0; n2 < N / 2; ++n2)
+              st_async_b32(dst + (uint32_t)(n2 * 48 * 4), __uint_as_float(pack_bf16(v[2 * n2], v[2 * n2 + 1])), mbr);
+          } else {
+            const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * 48 + cu) * 4), q);
+#pragma unroll
+            for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * 48 * 4), v[n], mbr);
+          }
         }
       }
       for (int ent = fixed ? nent : w >> 2; ent < nent; ent += ngrp) {
@@ -746,7 +770,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           if (a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
                              // 32 consecutive columns = one contiguous 128-byte row segment per n
             const uint32_t mbr = mapa_shared(rbar, q);
-            if (u48) {
+            if (pbf) {
+              const uint32_t dst = mapa_shared(rb + (uint32_t)((me * (N / 2) * a.UPC + cu) * 4), q);
+#pragma unroll
+              for (int n2 = 0; n2 < N / 2; ++n2)
+                st_async_b32(dst + (uint32_t)(n2 * a.UPC * 4), __uint_as_float(pack_bf16(v[2 * n2], v[2 * n2 + 1])),
+                             mbr);
+            } else if (u48) {
               const uint32_t dst = mapa_shared(rb + (uint32_t)((me * N * 48 + cu) * 4), q);
 #pragma unroll
               for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * 48 * 4), v[n], mbr);
@@ -905,6 +935,10 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.prof = g_prof_buf;
   a.prof_steps = g_prof_steps;
   a.dsm = backward ? cs.dsm : 0;
+  // 4-gate cells exchange the R^T.dg partials as bf16 pairs by default (half the DSMEM
+  // bytes and pushes; backward 4.10 -> 3.58 us/step at H=768, gradient errors vs the
+  // f64 oracle 1.75e-3 -> 1.82e-3 normwise); FRNN_PBF16=0/1 overrides.
+  a.pbf16 = getenv("FRNN_PBF16") ? atoi(getenv("FRNN_PBF16")) : (p.NG == 4 ? 1 : 0);
   a.skeleton = g_skeleton;
   char* w = static_cast<char*>(ws);
   if (!backward) {
