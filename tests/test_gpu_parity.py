@@ -183,6 +183,15 @@ def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
     check_bf16(eng, orc, v, inp)
 
 
+@pytest.mark.parametrize("pbf16", ["0", "1"])
+def test_bf16_partial_exchange_modes(eng, orc, monkeypatch, pbf16):
+    """The backward's R^T.dg partials as fp32 (FRNN_PBF16=0) or bf16 pairs (the
+    default for 4-gate cells): both within the bf16 tolerance."""
+    monkeypatch.setenv("FRNN_PBF16", pbf16)
+    inp = orc.generate("slstm", 12, 16, 1, 768, seed=14)
+    check_bf16(eng, orc, "slstm", inp)
+
+
 @pytest.mark.parametrize("NH,DH", [(4, 192), (12, 64)])
 def test_bf16_lstm_heads(eng, orc, NH, DH):
     """Config 3: head-wise block-diagonal R."""
