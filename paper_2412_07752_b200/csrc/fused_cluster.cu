@@ -678,6 +678,27 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           mma12_ts(acc + 3 * N, tbase + 3 * cb, bd, bk, idesc, 0);
           if (elect_one()) mma_commit(&blkbar[3]);
           __syncwarp();
+        } else if (MBT == 6 && MS == 0 && nk == 3 && !a.skeleton) {  // single-gate cells at H=768 (Elman)
+          const uint64_t bk = (2 * LBO) >> 4;
+          const uint32_t acc = tbase + a.acc1;
+          mma3_ts(acc, tbase, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[0]);
+          __syncwarp();
+          mma3_ts(acc + N, tbase + cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[1]);
+          __syncwarp();
+          mma3_ts(acc + 2 * N, tbase + 2 * cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[2]);
+          __syncwarp();
+          mma3_ts(acc + 3 * N, tbase + 3 * cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[3]);
+          __syncwarp();
+          mma3_ts(acc + 4 * N, tbase + 4 * cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[4]);
+          __syncwarp();
+          mma3_ts(acc + 5 * N, tbase + 5 * cb, bd, bk, idesc, 0);
+          if (elect_one()) mma_commit(&blkbar[5]);
+          __syncwarp();
         } else if (MBT == 2 && MS == 0 && nk == 12 && !a.skeleton) {  // DH=192 per head (config 3)
           const uint64_t bk = (2 * LBO) >> 4;
           mma12_ts(tbase + a.acc1, tbase, bd, bk, idesc, 0);

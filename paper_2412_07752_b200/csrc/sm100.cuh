@@ -211,6 +211,21 @@ __device__ __forceinline__ void mma8_ts(uint32_t d, uint32_t ta, uint64_t bd, ui
       "r"(ta), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
       : "memory");
 }
+// 3 TS steps (a K=48 block: the single-gate backward at UPC=48).
+__device__ __forceinline__ void mma3_ts(uint32_t d, uint32_t ta, uint64_t bd, uint64_t bk, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t" FRNN_MMA_HEAD("%5")
+      ".reg .b32 a;\n\t.reg .b64 b;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, p;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "add.u32 a, a, 8;\n\tadd.u64 b, b, %3;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %4, t;\n\t"
+      "}" ::"r"(d),
+      "r"(ta), "l"(bd), "l"(bk), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // operands: %0 d, %1 A (tmem address), %2 B desc, %3 idesc, %4 acc
 __device__ __forceinline__ void mma1_ts(uint32_t d, uint32_t ta, uint64_t bd, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -402,6 +417,10 @@ __device__ __forceinline__ void mma12_ts(uint32_t d, uint32_t ta, uint64_t bd, u
 __device__ __forceinline__ void mma_run_ts(uint32_t d, uint32_t a0, uint32_t a_step, uint64_t b0, uint64_t b_step,
                                            uint32_t idesc, int n, bool acc0 = false) {
   int k = 0;
+  if (a_step == 8 && n == 3) {
+    mma3_ts(d, a0, b0, b_step, idesc, acc0);
+    return;
+  }
   if (a_step == 8) {
     for (; k + 8 <= n; k += 8) mma8_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0 || acc0);
     for (; k + 4 <= n; k += 4) mma4_ts(d, a0 + 8u * k, b0 + (uint64_t)k * b_step, b_step, idesc, k > 0 || acc0);
