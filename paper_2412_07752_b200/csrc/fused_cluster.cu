@@ -363,6 +363,26 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   if (w == 0) tmem_dealloc(tbase, a.tmem_cols);
 }
 
+// Backward MMA issue for a tiling known at compile time: MBT TMEM-A blocks, MS
+// SMEM-A blocks of 128 columns (paired with the first MS TMEM blocks), NK K-steps
+// per block, N=16 -- every offset a constant, straight-line issue (the generic
+// runtime loop is markedly slower at N=16, see DESIGN 8c).
+template <int MBT_, int MS_, int NK>
+__device__ __noinline__ void issue_bwd_fixed(uint32_t tbase, uint32_t acc1, uint64_t bd, uint64_t ad, uint32_t idesc,
+                                                uint32_t idesc2, uint64_t* blkbar) {
+  constexpr int NP = MBT_ > MS_ ? MBT_ : MS_, CB = NK * 8;
+  constexpr uint64_t bk = (2 * 16 * 16) >> 4, a2k = (2 * 128 * 16) >> 4, blk16 = (uint64_t)128 * NK * 16 * 2 >> 4;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const uint32_t accT = acc1 + i * 16, accS = acc1 + (MBT_ + i) * 16;
+    if (i < MBT_ && i < MS_) mma_run_ts_ss(accT, tbase + i * CB, accS, ad + i * blk16, a2k, bd, bk, idesc, idesc2, NK);
+    else if (i < MBT_) mma_run_ts(accT, tbase + i * CB, 8, bd, bk, idesc, NK);
+    else mma_run_ss(accS, ad + i * blk16, a2k, bd, bk, idesc2, NK);
+    if (elect_one()) mma_commit(&blkbar[i]);
+    __syncwarp();
+  }
+}
+
 // ----------------------------------------------------------- backward ----
 template <int V, int N>
 __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
@@ -699,6 +719,14 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           mma3_ts(acc + 5 * N, tbase + 5 * cb, bd, bk, idesc, 0);
           if (elect_one()) mma_commit(&blkbar[5]);
           __syncwarp();
+        } else if (N == 16 && MBT == 5 && MS == 0 && nk == 10 && !a.skeleton) {  // e.g. H=640, 4 gates
+          issue_bwd_fixed<5, 0, 10>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
+        } else if (N == 16 && MBT == 4 && MS == 0 && nk == 8 && !a.skeleton) {  // e.g. H=512, 4 gates
+          issue_bwd_fixed<4, 0, 8>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
+        } else if (N == 16 && MBT == 3 && MS == 0 && nk == 12 && !a.skeleton) {  // e.g. 2 heads of 384
+          issue_bwd_fixed<3, 0, 12>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
+        } else if (N == 16 && SSM == 128 && MBT == 3 && MS == 4 && nk == 14 && !a.skeleton) {
+          issue_bwd_fixed<3, 4, 14>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
         } else if (MBT == 2 && MS == 0 && nk == 12 && !a.skeleton) {  // DH=192 per head (config 3)
           const uint64_t bk = (2 * LBO) >> 4;
           mma12_ts(tbase + a.acc1, tbase, bd, bk, idesc, 0);

@@ -174,7 +174,7 @@ def test_bf16_cluster_three_batch_tiles(eng, orc, v):
 
 
 @pytest.mark.parametrize("v,NH,DH,B", [("slstm", 1, 640, 24), ("slstm", 1, 896, 20), ("lstm", 2, 384, 24),
-                                       ("elman", 1, 512, 16)])
+                                       ("elman", 1, 512, 16), ("gru", 1, 512, 16)])
 def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
     """Head dims whose tilings differ from the headline: DH=640 (UPC=40, five
     TMEM blocks, no SMEM block), DH=896 (no cluster tiling: L2-flag fused
