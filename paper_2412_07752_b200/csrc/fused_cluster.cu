@@ -90,6 +90,17 @@ __device__ __forceinline__ uint32_t kmaj(int r, int k, int rows) {
   return (uint32_t)(((k >> 3) * (rows >> 3) + (r >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
 }
 
+// Forward MMA issue for K = 16*NK known at compile time (TMEM-A M=128 block
+// interleaved with the SMEM-A M=64 block), out of line like issue_bwd_fixed.
+template <int NK>
+__device__ __noinline__ void issue_fwd_fixed(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t a2, uint64_t bd,
+                                             uint32_t id1, uint32_t id2) {
+  constexpr uint64_t a2k = (2 * 64 * 16) >> 4, bk = (2 * 16 * 16) >> 4;
+#pragma unroll
+  for (int k = 0; k + 8 <= NK; k += 8)
+    mma8_ts_ss(d1, ta + 8u * k, d2, a2 + k * a2k, a2k, bd + k * bk, bk, id1, id2, k > 0);
+}
+
 // ------------------------------------------------------------ forward ----
 template <int V, int N>
 __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
@@ -229,6 +240,12 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         mma8_ts_ss(d1, tbase + 192, d2, a2 + 24 * a2k, a2k, bd + 24 * bk, bk, idesc1, idesc2, 1);
         mma8_ts_ss(d1, tbase + 256, d2, a2 + 32 * a2k, a2k, bd + 32 * bk, bk, idesc1, idesc2, 1);
         mma8_ts_ss(d1, tbase + 320, d2, a2 + 40 * a2k, a2k, bd + 40 * bk, bk, idesc1, idesc2, 1);
+      } else if (N == 16 && a.R2 && K == 640) {
+        issue_fwd_fixed<40>(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128), bd, idesc1,
+                            idesc2);
+      } else if (N == 16 && a.R2 && K == 512) {
+        issue_fwd_fixed<32>(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128), bd, idesc1,
+                            idesc2);
       } else if (a.R2 && K == 192) {  // DH=192 per head (config 3): one 12-step block
         mma12_ts_ss(tbase + a.acc1, tbase, tbase + a.acc2, sdesc_kmajor(smem_u32(A2), 64 * 16, 128),
                     (2 * 64 * 16) >> 4, bd, (2 * LBO) >> 4, idesc1, idesc2, 0);
