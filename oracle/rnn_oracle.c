@@ -15,7 +15,7 @@
  * Every function cites the reference file:line it restates.  Paths are
  * relative to /root/reference/proj/core/include/rnnkit/rnn/.
  *
- * Build: gcc -O2 -ffp-contract=off -fPIC -shared (see oracle/Makefile).  No
+ * Build: gcc -O3 -fopenmp -ffp-contract=off -fPIC -shared (oracle/Makefile).  No
  * FMA contraction, so float results are bit-identical to the reference
  * engine<float> compiled with the same flags.
  */
@@ -188,6 +188,25 @@ DEF_CELL(float, f, tanhf, expf)
 #define GIDX(t, j, b, e) ((((size_t)(t) * NG + (j)) * B + (b)) * D + (e))
 #define DSIDX(i, b, e) (((size_t)(i) * B + (b)) * D + (e))
 
+/* Loop orders.  Every output element below is produced by EXACTLY the
+ * sequence of floating-point operations the reference performs for it
+ * (same operands, same order, same rounding; -ffp-contract=off), so the
+ * results are bit-identical to the reference engine -- pinned by
+ * tests/test_oracle.py.  What differs is only which element is computed when:
+ *   - R.h (engine.hpp:178-182) keeps each gate's ascending-c sum but runs the
+ *     B sums of one R row side by side (h transposed to [D][B]), so R is read
+ *     once per step and the inner loop vectorises across b;
+ *   - R^T.dg (:291-305) keeps each column's (j ascending, r ascending) sum but
+ *     walks R row-major with the column accumulators in a [B][chunk] array;
+ *   - dR (:321-334) keeps each element's ascending-b sum in an accumulator
+ *     row before the single += into dR.
+ * Independent elements are spread over OpenMP threads (OMP_NUM_THREADS);
+ * nothing is reduced across threads, so the thread count
+ * never changes a bit.  This is what lets the checker run the headline
+ * shape (T=1024, B=16, H=768) in seconds.                                  */
+#define ORC_BT 16   /* batch rows per R.h register block   */
+#define ORC_CC 32   /* R^T.dg columns per task              */
+
 /* engine.hpp:143-203 forward (finiteness/shape checks are the caller's). */
 #define DEF_FWD(S, SUF, CS)                                                               \
   void orc_forward_##SUF(const orc_cell* cell, int T, int B, int NH, int DH,        \
@@ -195,33 +214,51 @@ DEF_CELL(float, f, tanhf, expf)
                          S* states, S* gates) {                                    \
     const int NS = cell->num_states, NG = cell->num_gates, D = NH * DH;             \
     memcpy(states, s0, sizeof(S) * (size_t)NS * B * D); /* :161-164 */             \
-    S prev[4], g[4], next[4];                                                      \
+    S* hT = (S*)malloc(sizeof(S) * (size_t)D * (B > 0 ? B : 1));                   \
     for (int t = 0; t < T; ++t) {                                                  \
       const S* sp0 = &states[SIDX(t, 0, 0, 0)];                                    \
+      _Pragma("omp parallel for schedule(static)")                                 \
+      for (int e = 0; e < D; ++e)                                                  \
+        for (int b = 0; b < B; ++b) hT[(size_t)e * B + b] = sp0[(size_t)b * D + e]; \
+      _Pragma("omp parallel for collapse(2) schedule(dynamic, 8)")                 \
       for (int j = 0; j < NG; ++j)                                                 \
-        for (int b = 0; b < B; ++b)                                                \
-          for (int hd = 0; hd < NH; ++hd)                                          \
-            for (int r = 0; r < DH; ++r) {                                         \
-              int e = hd * DH + r;                                                 \
-              S y = 0;                                                             \
-              if (cell->uses_rec[j]) { /* :178-182 ascending c */                 \
-                const S* row = &R[RIDX(hd, j, r, 0)];                              \
-                const S* sp = sp0 + (size_t)b * D + hd * DH;                       \
-                for (int c = 0; c < DH; ++c) y += row[c] * sp[c];                  \
+        for (int e = 0; e < D; ++e) {                                              \
+          const int hd = e / DH, r = e % DH;                                       \
+          for (int b0 = 0; b0 < B; b0 += ORC_BT) {                                 \
+            const int nb = B - b0 < ORC_BT ? B - b0 : ORC_BT;                       \
+            S y[ORC_BT];                                                           \
+            for (int k = 0; k < ORC_BT; ++k) y[k] = 0;                             \
+            if (cell->uses_rec[j]) { /* :178-182 ascending c */                   \
+              const S* row = &R[RIDX(hd, j, r, 0)];                                \
+              const S* hc = hT + (size_t)hd * DH * B + b0;                         \
+              if (nb == ORC_BT) {                                                  \
+                for (int c = 0; c < DH; ++c)                                       \
+                  for (int k = 0; k < ORC_BT; ++k) y[k] += row[c] * hc[(size_t)c * B + k]; \
+              } else {                                                             \
+                for (int c = 0; c < DH; ++c)                                       \
+                  for (int k = 0; k < nb; ++k) y[k] += row[c] * hc[(size_t)c * B + k]; \
               }                                                                    \
+            }                                                                      \
+            for (int k = 0; k < nb; ++k) {                                         \
+              const int b = b0 + k;                                                \
               S acc = cell->uses_in[j] ? x[XIDX(t, b, j, e)] : (S)0; /* :183-187 */ \
               acc += bias[(size_t)j * D + e];                                      \
-              acc += y;                                                            \
+              acc += y[k];                                                         \
               gates[GIDX(t, j, b, e)] = acc;                                       \
             }                                                                      \
-      for (int b = 0; b < B; ++b) /* :193-200 */                                   \
+          }                                                                        \
+        }                                                                          \
+      _Pragma("omp parallel for collapse(2) schedule(static)") /* :193-200 */     \
+      for (int b = 0; b < B; ++b)                                                  \
         for (int e = 0; e < D; ++e) {                                              \
+          S prev[4], g[4], next[4];                                                \
           for (int i = 0; i < NS; ++i) prev[i] = states[SIDX(t, i, b, e)];          \
           for (int j = 0; j < NG; ++j) g[j] = gates[GIDX(t, j, b, e)];              \
           pw_fwd_##CS(cell, prev, g, next);                                       \
           for (int i = 0; i < NS; ++i) states[SIDX(t + 1, i, b, e)] = next[i];      \
         }                                                                          \
     }                                                                              \
+    free(hT);                                                                      \
   }
 
 DEF_FWD(double, f64, d)
@@ -242,20 +279,21 @@ enum { ORC_CLIP_OFF = 0, ORC_CLIP_VALUE = 1, ORC_CLIP_ZERO = 2 };
     memset(dx, 0, sizeof(S) * (size_t)T * B * NG * D);                             \
     memset(dbias, 0, sizeof(S) * (size_t)NG * D);                                  \
     memset(dR, 0, sizeof(S) * (size_t)NH * NG * DH * DH);                          \
-    S* ds_cur = (S*)malloc(sizeof(S) * nst);                                       \
-    S* ds_prev = (S*)malloc(sizeof(S) * nst);                                      \
-    S* dg = (S*)malloc(sizeof(S) * (size_t)NG * B * D);                            \
+    S* ds_cur = (S*)malloc(sizeof(S) * (nst ? nst : 1));                           \
+    S* ds_prev = (S*)malloc(sizeof(S) * (nst ? nst : 1));                          \
+    S* dg = (S*)malloc(sizeof(S) * ((size_t)NG * B * D + 1));                      \
     memcpy(ds_cur, d_states_final, sizeof(S) * nst); /* :248 */                    \
     const S mag = (S)clip_mag; /* :255 */                                          \
-    S prev[4], g[4], dsl[4], Jg[4][4], Jp[4][4];                                   \
+    const int ncc = (DH + ORC_CC - 1) / ORC_CC;                                    \
     for (int t = T - 1; t >= 0; --t) {                                             \
       if (d_hidden) /* :258-263 */                                                 \
         for (int b = 0; b < B; ++b)                                                \
           for (int e = 0; e < D; ++e)                                              \
             ds_cur[DSIDX(0, b, e)] += d_hidden[((size_t)t * B + b) * D + e];        \
-      memset(ds_prev, 0, sizeof(S) * nst);                                         \
-      for (int b = 0; b < B; ++b) /* :267-286 */                                   \
+      _Pragma("omp parallel for collapse(2) schedule(static)") /* :267-286 */     \
+      for (int b = 0; b < B; ++b)                                                  \
         for (int e = 0; e < D; ++e) {                                              \
+          S prev[4], g[4], dsl[4], Jg[4][4], Jp[4][4];                             \
           for (int i = 0; i < NS; ++i) {                                           \
             prev[i] = states[SIDX(t, i, b, e)];                                    \
             dsl[i] = ds_cur[DSIDX(i, b, e)];                                       \
@@ -273,41 +311,59 @@ enum { ORC_CLIP_OFF = 0, ORC_CLIP_VALUE = 1, ORC_CLIP_ZERO = 2 };
             ds_prev[DSIDX(k, b, e)] = acc;                                         \
           }                                                                        \
         }                                                                          \
-      if (clip_mode != ORC_CLIP_ZERO) /* :289-308 */                               \
-        for (int b = 0; b < B; ++b)                                                \
-          for (int hd = 0; hd < NH; ++hd)                                          \
-            for (int c = 0; c < DH; ++c) {                                         \
-              S term = 0;                                                          \
-              for (int j = 0; j < NG; ++j) {                                       \
-                if (!cell->uses_rec[j]) continue;                                  \
-                const S* dgj = &dg[((size_t)j * B + b) * D + hd * DH];             \
-                for (int r = 0; r < DH; ++r) term += R[RIDX(hd, j, r, c)] * dgj[r]; \
+      if (clip_mode != ORC_CLIP_ZERO) { /* :289-308 */                             \
+        _Pragma("omp parallel for collapse(2) schedule(dynamic, 1)")               \
+        for (int hd = 0; hd < NH; ++hd)                                            \
+          for (int cc = 0; cc < ncc; ++cc) {                                       \
+            const int c0 = cc * ORC_CC;                                            \
+            const int nc = DH - c0 < ORC_CC ? DH - c0 : ORC_CC;                     \
+            S* term = (S*)calloc((size_t)B * ORC_CC, sizeof(S));                   \
+            for (int j = 0; j < NG; ++j) {                                         \
+              if (!cell->uses_rec[j]) continue;                                    \
+              for (int r = 0; r < DH; ++r) {                                       \
+                const S* Rr = &R[RIDX(hd, j, r, c0)];                              \
+                for (int b = 0; b < B; ++b) {                                      \
+                  const S d = dg[((size_t)j * B + b) * D + hd * DH + r];           \
+                  S* tb = term + (size_t)b * ORC_CC;                               \
+                  for (int c = 0; c < nc; ++c) tb[c] += Rr[c] * d;                 \
+                }                                                                  \
               }                                                                    \
-              if (clip_mode == ORC_CLIP_VALUE) {                                   \
-                if (term > mag) term = mag;                                        \
-                if (term < -mag) term = -mag;                                      \
-              }                                                                    \
-              ds_prev[DSIDX(0, b, hd * DH + c)] += term;                           \
             }                                                                      \
-      for (int j = 0; j < NG; ++j) /* :311-320 */                                  \
-        for (int b = 0; b < B; ++b)                                                \
-          for (int e = 0; e < D; ++e) {                                            \
+            for (int b = 0; b < B; ++b)                                            \
+              for (int c = 0; c < nc; ++c) {                                       \
+                S v = term[(size_t)b * ORC_CC + c];                                \
+                if (clip_mode == ORC_CLIP_VALUE) {                                 \
+                  if (v > mag) v = mag;                                            \
+                  if (v < -mag) v = -mag;                                          \
+                }                                                                  \
+                ds_prev[DSIDX(0, b, hd * DH + c0 + c)] += v;                       \
+              }                                                                    \
+            free(term);                                                            \
+          }                                                                        \
+      }                                                                            \
+      _Pragma("omp parallel for collapse(2) schedule(static)") /* :311-320 */     \
+      for (int j = 0; j < NG; ++j)                                                 \
+        for (int e = 0; e < D; ++e)                                                \
+          for (int b = 0; b < B; ++b) {                                            \
             S v = dg[((size_t)j * B + b) * D + e];                                 \
             if (cell->uses_in[j]) dx[XIDX(t, b, j, e)] = v;                        \
             dbias[(size_t)j * D + e] += v;                                         \
           }                                                                        \
-      for (int hd = 0; hd < NH; ++hd) /* :321-334 */                               \
-        for (int j = 0; j < NG; ++j) {                                             \
-          if (!cell->uses_rec[j]) continue;                                        \
-          for (int r = 0; r < DH; ++r)                                             \
-            for (int c = 0; c < DH; ++c) {                                         \
-              S acc = 0;                                                           \
-              for (int b = 0; b < B; ++b)                                          \
-                acc += dg[((size_t)j * B + b) * D + hd * DH + r] *                 \
-                       states[SIDX(t, 0, b, hd * DH + c)];                         \
-              dR[RIDX(hd, j, r, c)] += acc;                                        \
+      _Pragma("omp parallel for collapse(3) schedule(dynamic, 4)") /* :321-334 */ \
+      for (int hd = 0; hd < NH; ++hd)                                              \
+        for (int j = 0; j < NG; ++j)                                               \
+          for (int r = 0; r < DH; ++r) {                                           \
+            if (!cell->uses_rec[j]) continue;                                      \
+            S* acc = (S*)calloc((size_t)DH, sizeof(S));                            \
+            for (int b = 0; b < B; ++b) {                                          \
+              const S d = dg[((size_t)j * B + b) * D + hd * DH + r];               \
+              const S* h = &states[SIDX(t, 0, b, hd * DH)];                        \
+              for (int c = 0; c < DH; ++c) acc[c] += d * h[c];                     \
             }                                                                      \
-        }                                                                          \
+            S* out = &dR[RIDX(hd, j, r, 0)];                                       \
+            for (int c = 0; c < DH; ++c) out[c] += acc[c];                         \
+            free(acc);                                                             \
+          }                                                                        \
       S* tmp = ds_cur; ds_cur = ds_prev; ds_prev = tmp; /* :335 */                 \
     }                                                                              \
     memcpy(ds0, ds_cur, sizeof(S) * nst); /* :337 */                               \

@@ -147,11 +147,22 @@ class FlashRNN:
     def _opts(algo="auto", check_finite=False):
         return Options(FLAG_CHECK_FINITE if check_finite else 0, ALGO[algo])
 
-    def workspace(self, nbytes: int, device):
-        key = (str(device), threading.get_ident())
+    def workspace(self, nbytes: int, device, stream=None):
+        """Scratch for one call: cached per (device, stream, thread), so calls on
+        different streams never share flags / partial sums.  A grown buffer is
+        allocated on the caller's stream (torch's caching allocator then keeps
+        the old one from being reused before that stream's work is done)."""
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(device).cuda_stream
+        key = (str(device), int(s or 0), threading.get_ident())
         buf = self._ws.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = self.torch.empty(max(nbytes, 256), dtype=self.torch.uint8, device=device)
+            ext = torch.cuda.ExternalStream(s, device=device) if s else torch.cuda.default_stream(device)
+            old = buf
+            with torch.cuda.stream(ext):
+                buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            if old is not None:
+                old.record_stream(ext)
             self._ws[key] = buf
         return buf
 
@@ -184,8 +195,8 @@ class FlashRNN:
         o = self._opts(algo, check_finite)
         n = C.c_size_t()
         _check(self.lib.frnn_workspace_size(C.byref(cell), shape, dt, 0, C.byref(o), C.byref(n)))
-        ws = self.workspace(n.value, R.device)
         s = stream if stream is not None else torch.cuda.current_stream(R.device).cuda_stream
+        ws = self.workspace(n.value, R.device, s)
         _check(self.lib.frnn_forward(C.byref(cell), shape, dt, R.data_ptr(), bias.data_ptr(),
                                      x.data_ptr(), s0.data_ptr(), states.data_ptr(),
                                      gates.data_ptr(), ws.data_ptr(), ws.numel(), C.byref(o), s))
@@ -225,8 +236,8 @@ class FlashRNN:
         o = self._opts(algo)
         n = C.c_size_t()
         _check(self.lib.frnn_workspace_size(C.byref(cell), shape, dt, 1, C.byref(o), C.byref(n)))
-        ws = self.workspace(n.value, R.device)
         s = stream if stream is not None else torch.cuda.current_stream(R.device).cuda_stream
+        ws = self.workspace(n.value, R.device, s)
         _check(self.lib.frnn_backward(
             C.byref(cell), shape, dt, R.data_ptr(), bias.data_ptr(), states.data_ptr(),
             gates.data_ptr(), d_states_final.data_ptr(),

@@ -13,6 +13,8 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <initializer_list>
+#include <utility>
 
 #include "../../include/flashrnn.h"
 #include "../../include/flashrnn_debug.h"
@@ -71,6 +73,22 @@ int validate(const frnn_cell* cell, const frnn_shape& s, int dtype) {
   return FRNN_OK;
 }
 
+int validate_pass(int32_t pass) {
+  if (pass != FRNN_PASS_FORWARD && pass != FRNN_PASS_BACKWARD)
+    return fail(FRNN_EINVAL_ARG, "pass must be FRNN_PASS_FORWARD (0) or FRNN_PASS_BACKWARD (1)");
+  return FRNN_OK;
+}
+
+// The kernels move R/s0/state rows with 16-byte vector loads and TMA (16-byte
+// aligned global addresses), so every tensor base must be 16-byte aligned; a
+// sliced tensor that is not would fault inside a kernel and poison the context.
+int check_aligned(std::initializer_list<std::pair<const void*, const char*>> ptrs) {
+  for (const auto& pr : ptrs)
+    if (pr.first && (reinterpret_cast<uintptr_t>(pr.first) & 15u))
+      return fail(FRNN_EINVAL_ARG, std::string(pr.second) + " is not 16-byte aligned");
+  return FRNN_OK;
+}
+
 int check_device() {
   static std::once_flag once;
   static int status = FRNN_OK;
@@ -83,7 +101,7 @@ int check_device() {
     if (e != cudaSuccess) {
       status = FRNN_ECUDA;
       msg = std::string("no CUDA device: ") + cudaGetErrorString(e);
-    } else if (prop.major != 10) {
+    } else if (prop.major != 10 || prop.minor != 0) {  // the fatbin carries sm_100a SASS only
       status = FRNN_ECUDA;
       msg = "libflashrnn is built for sm_100a (B200); found sm_" + std::to_string(prop.major * 10 + prop.minor);
     }
@@ -194,8 +212,19 @@ bool parse_plan_line(const std::string& line, int dev, Key* k, frnn::Plan* pl) {
   pl->ka = (int)v[27];
   pl->stages = (int)v[28];
   pl->ffma = (int)v[29];
-  pl->ws_bytes = (size_t)v[30];
   pl->solve_us = v[31];
+  // never trust the persisted size: the kernels' workspace layout may have
+  // changed since the line was written (recomputed from the plan's fields)
+  const int var = (int)v[5];
+  if (var < FRNN_ELMAN || var > FRNN_SLSTM || (int)v[13] < 0 || (int)v[13] > 1) return false;
+  frnn_cell cell = spec_of(var);
+  for (int j = 0; j < 4; ++j) {
+    cell.uses_recurrent[j] = ((int)v[6] >> j) & 1;
+    cell.uses_input[j] = ((int)v[7] >> j) & 1;
+  }
+  const frnn_shape sh{(int)v[8], (int)v[9], (int)v[10], (int)v[11]};
+  if (sh.seq_len < 0 || sh.batch < 1 || sh.num_heads < 1 || sh.head_dim < 1) return false;
+  pl->ws_bytes = frnn::plan_workspace(make_problem(&cell, sh, (int)v[12] ? FRNN_BF16 : FRNN_F32), (int)v[13], *pl);
   return true;
 }
 
@@ -299,6 +328,7 @@ int frnn_plan(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pa
   g_err.clear();
   int rc = validate(cell, shape, dtype);
   if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
   if (!out) return fail(FRNN_EINVAL_ARG, "null output");
   frnn::Problem p = make_problem(cell, shape, dtype);
   frnn::Plan pl{};
@@ -353,6 +383,7 @@ int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32
   g_err.clear();
   int rc = validate(cell, shape, dtype);
   if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
   frnn::Problem p = make_problem(cell, shape, dtype);
   frnn::Plan pl{};
   if ((rc = get_plan(p, pass, opts, &pl))) return rc;
@@ -386,6 +417,7 @@ int frnn_workspace_size(const frnn_cell* cell, frnn_shape shape, int32_t dtype, 
   g_err.clear();
   int rc = validate(cell, shape, dtype);
   if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
   if (!bytes) return fail(FRNN_EINVAL_ARG, "null output");
   frnn::Problem p = make_problem(cell, shape, dtype);
   frnn::Plan pl{};
@@ -402,6 +434,9 @@ int frnn_forward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const v
   if (rc) return rc;
   if (!R || !bias || !s0 || !states || (shape.seq_len > 0 && (!x || !gates)))
     return fail(FRNN_EINVAL_ARG, "null tensor pointer");
+  if ((rc = check_aligned({{R, "R"}, {bias, "bias"}, {x, "x"}, {s0, "s0"}, {states, "states"}, {gates, "gates"},
+                           {workspace, "workspace"}})))
+    return rc;
   if ((rc = check_device())) return rc;
   frnn::Problem p = make_problem(cell, shape, dtype);
   p.R = R; p.bias = bias; p.x = x; p.s0 = s0; p.states = states; p.gates = gates;
@@ -455,6 +490,10 @@ int frnn_backward(const frnn_cell* cell, frnn_shape shape, int32_t dtype, const 
   if (clip.mode < FRNN_CLIP_OFF || clip.mode > FRNN_CLIP_ZERO) return fail(FRNN_EINVAL_ARG, "bad clip mode");
   if (!R || !states || !d_states_final || !dbias || !dR || !ds0 || (shape.seq_len > 0 && (!gates || !dx)))
     return fail(FRNN_EINVAL_ARG, "null tensor pointer");
+  if ((rc = check_aligned({{R, "R"}, {bias, "bias"}, {states, "states"}, {gates, "gates"},
+                           {d_states_final, "d_states_final"}, {d_hidden, "d_hidden"}, {dx, "dx"},
+                           {dbias, "dbias"}, {dR, "dR"}, {ds0, "ds0"}, {workspace, "workspace"}})))
+    return rc;
   if ((rc = check_device())) return rc;
   frnn::Problem p = make_problem(cell, shape, dtype);
   p.R = R; p.bias = bias; p.cstates = states; p.cgates = gates; p.dsf = d_states_final; p.dh = d_hidden;
@@ -495,7 +534,9 @@ int frnn_input_projection(const void* W, const void* u, void* x, int64_t tokens,
   if (tokens < 1 || out_features < 1 || in_features < 1) return fail(FRNN_EINVAL_SHAPE, "degenerate shape");
   if (dtype != FRNN_BF16) return fail(FRNN_EUNSUPPORTED, "input projection: bf16 only");
   if (in_features % 8) return fail(FRNN_EINVAL_SHAPE, "in_features must be a multiple of 8 (16-byte TMA rows)");
-  int rc = check_device();
+  int rc = check_aligned({{W, "W"}, {u, "u"}, {x, "x"}});
+  if (rc) return rc;
+  rc = check_device();
   if (rc) return rc;
   cudaError_t e = frnn::wx_gemm(W, u, x, tokens, out_features, in_features, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported) return fail(FRNN_EUNSUPPORTED, "TMA tensor maps unavailable");

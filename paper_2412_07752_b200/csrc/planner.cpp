@@ -371,6 +371,23 @@ void plan_ffma(const Problem& p, int pass, Plan* out) {
 
 }  // namespace
 
+size_t plan_workspace(const Problem& p, int pass, const Plan& pl) {
+  switch (pl.algo) {
+    case FRNN_ALGO_SIMT: {
+      Plan q{};
+      std::string why;
+      plan_simt(p, pass, device_limits(), &q, &why);
+      return q.ws_bytes;
+    }
+    case FRNN_ALGO_FUSED:
+      if (pl.cluster) return pass == 0 ? cluster_forward_ws(p, pl) : cluster_backward_ws(p, pl);
+      return pass == 0 ? fused_forward_ws(p, pl) : fused_backward_ws(p, pl);
+    default:
+      if (pl.ffma) return pass == 0 ? alt32_forward_ws(p) : alt32_backward_ws(p);
+      return pass == 0 ? alt_forward_ws(p, pl) : alt_backward_ws(p, pl);
+  }
+}
+
 std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimits& lim) {
   if (algo == FRNN_ALGO_ALTERNATING) return csp::format(alt_csp(p, pass, lim).p);
   return csp::format(cluster_csp(p, pass, lim, 0).p);

@@ -28,6 +28,10 @@ int solve_plan(const Problem& p, int pass, int algo_request, const DeviceLimits&
 
 // The tiling CSP of a kernel family (FRNN_ALGO_FUSED: cluster-resident kernels,
 // FRNN_ALGO_ALTERNATING) in the text form of include/flashrnn_csp.h.
+// Workspace bytes the kernels of `pl` carve up for problem `p` (recomputed from
+// the plan's fields, so a persisted plan never carries a stale size).
+size_t plan_workspace(const Problem& p, int pass, const Plan& pl);
+
 std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimits& lim);
 
 }  // namespace frnn

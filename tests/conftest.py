@@ -46,3 +46,30 @@ def rel_floor(a, b, floor):
     if a.size == 0:
         return 0.0
     return float(np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)))
+
+
+def trace_control(orc, v, R, states, gates, dsf, target_err, realizations=8, clip="off", mag=0.0,
+                  dh=None, seed=0):
+    """Sensitivity of the f64 backward (engine.hpp:221-339) to a bf16-level
+    change of its trace -- the CONTROL the sLSTM end-to-end gradient bound is
+    tied to.  The trace (states, gates of the f64 oracle forward) is perturbed
+    multiplicatively and rounded to bf16 (scalar.hpp:20-27) so that its
+    normwise distance from the f64 trace equals ``target_err`` (the GPU
+    forward's measured trace error; plain rounding when that is smaller), and
+    the oracle backward on each perturbed trace is compared with the one on
+    the f64 trace.  Returns {grad: max over realizations} and the per-
+    realization list.  Smooth cells give ~1e-3; sLSTM's Jacobian switches
+    branch at the stabiliser tie (cell.hpp:153), so near-tie elements flip and
+    the spread over realizations is wide at small T (few elements)."""
+    exact = orc.backward(v, R, states, gates, dsf, clip, mag, dh)
+    base = max(normwise(orc.round_bf16(states), states), 1e-30)
+    sc = float(np.sqrt(max(target_err ** 2 - base ** 2, 0.0)))
+    rs = np.random.RandomState(seed)
+    runs = []
+    for k in range(realizations):
+        noise = sc if k else 0.0  # realization 0: plain bf16 rounding
+        st = orc.round_bf16(states * (1 + noise * rs.standard_normal(states.shape)))
+        ga = orc.round_bf16(gates * (1 + noise * rs.standard_normal(gates.shape)))
+        g = orc.backward(v, R, st, ga, dsf, clip, mag, dh)
+        runs.append({key: normwise(g[key], exact[key]) for key in exact})
+    return {key: max(r[key] for r in runs) for key in exact}, runs

@@ -49,7 +49,7 @@ def test_version_and_cell_specs():
         assert list(c.uses_recurrent[:ng]) == rec and list(c.uses_input[:ng]) == inp
 
 
-def _fwd(cell, shape, dtype=1, ptr=1, ws=1 << 30, opts=None):
+def _fwd(cell, shape, dtype=1, ptr=256, ws=1 << 30, opts=None):
     L = load()
     p = C.c_void_p(ptr)
     return L.frnn_forward(C.byref(cell), shape, dtype, p, p, p, p, p, p, p, ws, opts, None)
@@ -68,10 +68,35 @@ def test_validation_mirrors_reference_errors():
     assert _fwd(c, Shape(4, 2, 1, 8), dtype=7) == 3  # unsupported dtype
     assert _fwd(c, Shape(4, 2, 1, 8), ptr=0) == 6  # null tensor
     # clip magnitude must be positive (engine.hpp:107)
-    p = C.c_void_p(1)
+    p = C.c_void_p(256)
     rc = L.frnn_backward(C.byref(c), Shape(4, 2, 1, 8), 1, p, p, p, p, p, None, Clip(1, 0.0), p, p, p, p, p,
                          1 << 30, None, None)
     assert rc == 6 and b"positive" in L.frnn_last_error()
+
+
+def test_misaligned_pointers_rejected():
+    """The kernels move rows with 16-byte loads / TMA: a tensor base that is not
+    16-byte aligned (e.g. a sliced tensor) is an argument error, checked before
+    any device work."""
+    L = load()
+    c = cell_spec("lstm")
+    assert _fwd(c, Shape(4, 2, 1, 8), ptr=256 + 2) == 6
+    assert b"16-byte aligned" in L.frnn_last_error()
+    p, q = C.c_void_p(256), C.c_void_p(256 + 8)
+    rc = L.frnn_backward(C.byref(c), Shape(4, 2, 1, 8), 1, p, p, p, p, p, None, Clip(0, 0.0), p, p, q, p, p,
+                         1 << 30, None, None)
+    assert rc == 6 and b"dR is not 16-byte aligned" in L.frnn_last_error()
+
+
+def test_pass_validated():
+    L = load()
+    info = PlanInfo()
+    n = C.c_size_t()
+    for bad in (2, -1):
+        assert L.frnn_plan(C.byref(cell_spec("lstm")), Shape(8, 4, 1, 64), 1, bad, None, C.byref(info)) == 6
+        assert b"pass" in L.frnn_last_error()
+        assert L.frnn_workspace_size(C.byref(cell_spec("lstm")), Shape(8, 4, 1, 64), 1, bad, None,
+                                     C.byref(n)) == 6
 
 
 def test_no_cpu_fallback_without_gpu():

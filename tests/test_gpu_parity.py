@@ -13,20 +13,25 @@ Tolerances (stated here and in DESIGN.md section 6):
       - end to end (oracle trace): same 2e-2 for Elman/LSTM/GRU.  The sLSTM
         gradient is discontinuous at the stabilizer tie a == i (the max branch,
         cell.hpp:153), so bf16-level differences in the trace flip a handful of
-        near-tie elements (~2e-5 of them) and move the normwise gradient error to
-        ~5-20%; its end-to-end error is reported and bounded at SLSTM_E2E_BOUND.
+        near-tie elements and move the normwise gradient error by what the bf16
+        format alone costs.  That cost is measured per case as the CONTROL
+        (conftest.trace_control): the oracle's own backward on its f64 trace
+        perturbed to the GPU trace's measured distance and rounded to bf16, vs
+        on the f64 trace, max over 8 realizations (the plain-rounding control
+        is pinned on the CPU by tests/test_oracle.py::test_bf16_trace_control);
+        sLSTM end to end is bounded by 2e-2 + control per gradient.
+    Full-length (T=1024) versions of these checks: tests/test_full_length_parity.py.
 """
 import numpy as np
 import pytest
 
-from conftest import normwise
+from conftest import normwise, trace_control
 
 pytestmark = pytest.mark.gpu
 
 VARIANTS = ["elman", "lstm", "gru", "slstm"]
 FP32_TOL = 1e-5
 BF16_TOL = 2e-2
-SLSTM_E2E_BOUND = 0.3
 GRADS = ("dx", "dbias", "dR", "ds0")
 
 
@@ -86,7 +91,11 @@ def check_bf16(eng, orc, v, inp, clip="off", mag=0.0, dh=None, algo="auto"):
     bwd = assert_close(gpu, cond, BF16_TOL, GRADS)
     e2e = {k: normwise(gpu[k], ora[k]) for k in GRADS}
     if v == "slstm":
-        assert max(e2e.values()) <= SLSTM_E2E_BOUND, e2e
+        ctl, _ = trace_control(orc, v, r["R"], ora["states"], ora["gates"], r["dsf"],
+                               fwd["states"], 8, clip, mag,
+                               orc.round_bf16(dh) if dh is not None else None)
+        bad = {k: (e2e[k], ctl[k]) for k in GRADS if not e2e[k] <= BF16_TOL + ctl[k]}
+        assert not bad, ("sLSTM end to end above control + 2e-2", bad)
     else:
         assert max(e2e.values()) <= BF16_TOL, e2e
     print(v, "fwd", fwd, "bwd(same trace)", bwd, "e2e", e2e)
