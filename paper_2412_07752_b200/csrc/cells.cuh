@@ -68,6 +68,15 @@ struct Math {
 
 // Compile-time cell traits.  NGP = gate rows per hidden unit in the tensor-core
 // tiles (all NG gates, padded to a power of two).
+//
+// Split backward (bf16 cluster kernels): coef<M>(prev, g, k) evaluates every
+// transcendental of the Jacobian (cell.hpp:108-201) from the trace alone into
+// NK coefficients, and apply(k, ds, dg, dsp) contracts them with the state
+// gradient (engine.hpp:275-284) in a few FMAs.  coef does not depend on ds,
+// so the kernel forms it for step t-1 while step t's MMAs run; apply is the
+// only cell work left between the partial exchange and the next MMA.  The
+// contraction is the chain rule through the cell's forward map, algebraically
+// equal to J^T ds (reassociated: bf16 mode only; the fp32 paths keep bwd).
 template <int V>
 struct Cell;
 
@@ -85,6 +94,16 @@ struct Cell<kElman> {
                                              float* dg, float* dsp) {
     float t = M::th(g[0]);
     dg[0] = (1.f - t * t) * ds[0];  // cell.hpp:114-117
+    dsp[0] = 0.f;
+  }
+  static constexpr int NK = 1;
+  template <class M>
+  static __device__ __forceinline__ void coef(const float* p, const float* g, float* k) {
+    const float t = M::th(g[0]);
+    k[0] = 1.f - t * t;
+  }
+  static __device__ __forceinline__ void apply(const float* k, const float* ds, float* dg, float* dsp) {
+    dg[0] = k[0] * ds[0];
     dsp[0] = 0.f;
   }
 };
@@ -124,6 +143,30 @@ struct Cell<kLstm> {
     dsp[0] = 0.f;
     dsp[1] = P01 * ds[0] + P11 * ds[1];
   }
+  // k = {so*(1-tanh^2 c), dc/dz, dc/df, dc/di, dh/do, sf}: dc_tot = ds_c + k0*ds_h
+  // carries the whole c path (J0j = so*dtc*J1j, P01 = so*dtc*sf)
+  static constexpr int NK = 6;
+  template <class M>
+  static __device__ __forceinline__ void coef(const float* p, const float* g, float* k) {
+    const float sf = M::sig(g[1]), si = M::sig(g[2]), so = M::sig(g[3]);
+    const float tz = M::th(g[0]);
+    const float tc = M::th(sf * p[1] + si * tz);
+    k[0] = so * (1.f - tc * tc);
+    k[1] = si * (1.f - tz * tz);
+    k[2] = sf * (1.f - sf) * p[1];
+    k[3] = si * (1.f - si) * tz;
+    k[4] = so * (1.f - so) * tc;
+    k[5] = sf;
+  }
+  static __device__ __forceinline__ void apply(const float* k, const float* ds, float* dg, float* dsp) {
+    const float dc = fmaf(k[0], ds[0], ds[1]);
+    dg[0] = k[1] * dc;
+    dg[1] = k[2] * dc;
+    dg[2] = k[3] * dc;
+    dg[3] = k[4] * ds[0];
+    dsp[0] = 0.f;
+    dsp[1] = k[5] * dc;
+  }
 };
 
 template <>
@@ -153,6 +196,24 @@ struct Cell<kGru> {
     dg[2] = omz * dtu * ds[0];
     dg[3] = omz * dtu * sr * (1.f - tg * tg) * ds[0];
     dsp[0] = sz * ds[0];
+  }
+  static constexpr int NK = 5;  // every gradient is a multiple of ds_h
+  template <class M>
+  static __device__ __forceinline__ void coef(const float* p, const float* g, float* k) {
+    const float sz = M::sig(g[0]), sr = M::sig(g[1]);
+    const float tg = M::th(g[3]);
+    const float tu = M::th(g[2] + sr * tg);
+    const float od = (1.f - sz) * (1.f - tu * tu);
+    k[0] = sz * (1.f - sz) * (p[0] - tu);
+    k[1] = od * sr * (1.f - sr) * tg;
+    k[2] = od;
+    k[3] = od * sr * (1.f - tg * tg);
+    k[4] = sz;
+  }
+  static __device__ __forceinline__ void apply(const float* k, const float* ds, float* dg, float* dsp) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dg[j] = k[j] * ds[0];
+    dsp[0] = k[4] * ds[0];
   }
 };
 
@@ -229,6 +290,53 @@ struct Cell<kSlstm> {
     dsp[1] = P01 * ds[0] + P11 * ds[1];
     dsp[2] = P02 * ds[0] + P22 * ds[2];
     dsp[3] = P03 * ds[0] + P13 * ds[1] + P23 * ds[2] + P33 * ds[3];
+  }
+  // Chain rule through h = so*c/n, c = fe*c' + ie*tz, n = fe*n' + ie, fe = e^(a-m),
+  // ie = e^(i-m), m = max(a, i) (ties -> a, cell.hpp:153), a = logsig(f) + m':
+  // dc = ds_c + ds_h*so/n, dn = ds_n - ds_h*so*c/n^2, dm = ds_m - fe*dfe - ie*die,
+  // da = fe*dfe + [a wins]*dm = dm', df = (1-sf)*da, di = ds_m - da.  Equal to
+  // the J^T ds of cell.hpp:150-198 (J11 = (1-sf)*P13, J12 = -P13, J01 = (1-sf)*P03 ...).
+  // k = {so/n, c/n, c', n', tz, fe, ie, ie*(1-tz^2), [a wins], 1-sf, so*(1-so)*c/n}
+  static constexpr int NK = 11;
+  template <class M>
+  static __device__ __forceinline__ void coef(const float* p, const float* g, float* k) {
+    const float sf = M::sig(g[1]), so = M::sig(g[3]);
+    const float a = M::logsig(g[1]) + p[3];
+    const bool use_a = !(a < g[2]);
+    const float e = M::ex(use_a ? g[2] - a : a - g[2]);
+    const float fexp = use_a ? 1.f : e, iexp = use_a ? e : 1.f;
+    const float tz = M::th(g[0]);
+    const float c = fexp * p[1] + iexp * tz;
+    const float inv_n = M::rcp(fexp * p[2] + iexp);
+    const float hov = c * inv_n;
+    k[0] = so * inv_n;
+    k[1] = hov;
+    k[2] = p[1];
+    k[3] = p[2];
+    k[4] = tz;
+    k[5] = fexp;
+    k[6] = iexp;
+    k[7] = iexp * (1.f - tz * tz);
+    k[8] = use_a ? 1.f : 0.f;
+    k[9] = 1.f - sf;
+    k[10] = so * (1.f - so) * hov;
+  }
+  static __device__ __forceinline__ void apply(const float* k, const float* ds, float* dg, float* dsp) {
+    const float q = ds[0] * k[0];
+    const float dc = ds[1] + q;
+    const float dn = fmaf(-q, k[1], ds[2]);
+    const float ef = (dc * k[2] + dn * k[3]) * k[5];
+    const float ei = (dc * k[4] + dn) * k[6];
+    const float dm = ds[3] - ef - ei;
+    const float da = fmaf(dm, k[8], ef);
+    dg[0] = dc * k[7];
+    dg[1] = da * k[9];
+    dg[2] = ds[3] - da;
+    dg[3] = ds[0] * k[10];
+    dsp[0] = 0.f;
+    dsp[1] = dc * k[5];
+    dsp[2] = dn * k[5];
+    dsp[3] = da;
   }
 };
 

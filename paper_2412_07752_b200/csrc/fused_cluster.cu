@@ -67,13 +67,18 @@ struct CArgs {
   int prof_steps;
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
+  int dxearly;     // store dx inside the MMA window (after the Jacobian) -- A/B knob FRNN_DXEARLY
+  int absu;        // absorb: CL == 16 unrolled (all loads first) -- A/B knob FRNN_ABSU
+  int pvec;        // pbf16: [cu/2][n/2][2] layout, two 16-byte pushes per lane (push_pair_cols);
+                   //        0 = [n/2][cu] layout, N/2 4-byte pushes per lane
   int skeleton;    // 1: synchronisation skeleton only -- no MMAs, no cell math (the sequential-
                    //    dependency floor of SURVEY 8d; frnn_debug_skeleton, results are garbage)
 };
 
-#define FRNN_PROF(slot, step)                                              \
-  if (a.prof && threadIdx.x == 0 && (step) < a.prof_steps)                 \
+#define FRNN_PROF_AT(slot, step, thr)                                      \
+  if (a.prof && threadIdx.x == (thr) && (step) < a.prof_steps)             \
     a.prof[((size_t)blockIdx.x * a.prof_steps + (step)) * 8 + (slot)] = clock64();
+#define FRNN_PROF(slot, step) FRNN_PROF_AT(slot, step, 0)
 
 __device__ __forceinline__ float bf(const bf16* p, size_t i) { return __bfloat162float(p[i]); }
 __host__ __device__ constexpr int xs_row(int r) { return r + 4 * (r >> 5); }
@@ -83,6 +88,73 @@ __device__ __forceinline__ float hi16(uint32_t v) { return __uint_as_float(v & 0
 __device__ __forceinline__ uint32_t ld2(const bf16* p, size_t i) { return *reinterpret_cast<const uint32_t*>(p + i); }
 __device__ __forceinline__ void st2(bf16* p, size_t i, float lo, float hi) {
   *reinterpret_cast<uint32_t*>(p + i) = pack_bf16(lo, hi);
+}
+
+// Element ownership: thread tid owns the unit pair (u, u+1) of batch row b.
+// Eight consecutive threads take eight consecutive rows b of the same pair, so
+// their 16-byte (backward dg) / 4-byte (forward h) stores into a K-major tile
+// land in the eight distinct 16-byte rows of one core matrix: no bank conflicts.
+// (Trace/x loads of a warp then touch 8 rows x 16 B -- off the critical path.)
+__device__ __forceinline__ void own_pair(int tid, int NP, int& u, int& b) {
+  u = 2 * ((tid >> 3) % NP);
+  b = (tid & 7) + 8 * (tid / (8 * NP));
+}
+
+// Backward partial exchange, bf16 pairs.  The receive block of source CTA `me`
+// in the owner's recv buffer is laid out [cu/2][n/2][2] (32-bit words: the bf16
+// pair (n, n+1) of column cu at word ((cu/2)*(N/2) + n/2)*2 + (cu&1)), so that
+//  * a drain lane (one column cu, N accumulator rows in v) and its neighbour
+//    lane (column cu^1) swap half their packed words with 4 shuffles and each
+//    push 32 contiguous bytes -- two st.async.v4 instead of N/2 scalar pushes;
+//  * the owner thread of units (u, u+1), batch row b, reads one 8-byte word
+//    pair per source, and 8 threads (b = 0..7) read 32 contiguous bytes.
+// Whole warp (the shuffles); `ok` guards the push (lanes pair up: cu even on
+// even lanes, UPC even).
+template <int N>
+__device__ __forceinline__ void push_pair_cols(const float* v, int lane, bool ok, int cu, uint32_t rb_me,
+                                               uint32_t q, uint32_t mbr) {
+  static_assert(N == 16, "bf16-pair exchange layout assumes N = 16");
+  uint32_t w[8], o[8];
+#pragma unroll
+  for (int n2 = 0; n2 < 8; ++n2) w[n2] = pack_bf16(v[2 * n2], v[2 * n2 + 1]);
+  const bool odd = lane & 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t got = __shfl_xor_sync(0xffffffffu, odd ? w[i] : w[4 + i], 1);
+    o[2 * i] = odd ? got : w[i];
+    o[2 * i + 1] = odd ? w[4 + i] : got;
+  }
+  if (ok) {
+    const uint32_t dst = mapa_shared(rb_me + (uint32_t)(((cu >> 1) * 16 + (odd ? 8 : 0)) * 4), q);
+    st_async_v4_b32(dst, o[0], o[1], o[2], o[3], mbr);
+    st_async_v4_b32(dst + 16, o[4], o[5], o[6], o[7], mbr);
+  }
+}
+
+// pvec 2: receive block [n][PW] of 32-bit words, word (n, cu/2) = bf16 pair
+// (column cu even, cu+1) of batch row n; PW = UPC/2 rounded up to 4 mod 8 so
+// that 8 owner threads (rows b..b+7, same unit pair) hit 8 distinct bank
+// groups.  A drain lane and its neighbour (columns cu, cu^1) swap 8 values so
+// the even lane holds rows 0..N/2-1 of the column pair and the odd lane rows
+// N/2..N-1; each pushes N/2 words.  The owner reads ONE word per source (no
+// half-used words: half the shared-memory traffic of the [n/2][cu] layout).
+__host__ __device__ constexpr int pair_pitch(int upc) { return ((upc / 2 + 3) / 8) * 8 + 4; }
+template <int N>
+__device__ __forceinline__ void push_col_pairs(const float* v, int lane, bool ok, int cu, int PW, uint32_t rb_me,
+                                               uint32_t q, uint32_t mbr) {
+  constexpr int H = N / 2;
+  const bool odd = lane & 1;
+  uint32_t w[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const float got = __shfl_xor_sync(0xffffffffu, odd ? v[i] : v[H + i], 1);
+    w[i] = odd ? pack_bf16(got, v[H + i]) : pack_bf16(v[i], got);
+  }
+  if (ok) {
+    const uint32_t dst = mapa_shared(rb_me + (uint32_t)(((odd ? H : 0) * PW + (cu >> 1)) * 4), q);
+#pragma unroll
+    for (int i = 0; i < H; ++i) st_async_b32(dst + (uint32_t)(i * PW * 4), __uint_as_float(w[i]), mbr);
+  }
 }
 
 // K-major, no-swizzle operand tile with `rows` rows: core matrix (k/8, r/8).
@@ -177,7 +249,8 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   // ---- element ownership: one pair (u, u+1) of one batch row b per thread
   const int NP = a.UPC / 2;
   const bool own = tid < NP * N;
-  const int u = 2 * (tid % NP), b = tid / NP;
+  int u, b;
+  own_pair(tid, NP, u, b);
   const bool valid = own && b < nb;
   const int e = hd * DH + unit0 + u;
   const size_t so = (size_t)(b0 + b) * D + e;       // offset in [.][B][D] tensors
@@ -423,8 +496,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const bf16* dh = static_cast<const bf16*>(p.dh);
   bf16* dx = static_cast<bf16*>(p.dx);
   bf16* ds0 = static_cast<bf16*>(p.ds0);
-  const bool pbf = a.pbf16 && a.dsm == 2;  // partials exchanged as bf16 pairs (n, n+1)
-  const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * (pbf ? 2 : 4);
+  const bool pbf = a.pbf16 && a.dsm == 2;  // partials exchanged as bf16 pairs
+  const int PW = pair_pitch(a.UPC);        // pvec 2 receive row pitch (words)
+  const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * (pbf ? 2 : 4);  // exchanged bytes (expect_tx)
+  const uint32_t recv_span = pbf && a.pvec == 2 ? (uint32_t)a.CL * N * PW * 4 : recv_bytes;  // buffer bytes
   const int MS = a.MS, SSM = a.SSM, NPAIR = max(MBT, MS);
   const size_t blk_bytes = (size_t)SSM * KBP * 2;  // one SMEM-A block
 
@@ -433,8 +508,8 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const int TP = a.UPC + 2;                                              // term pitch (bank spread)
   uint8_t* AS = smem;                                                    // MS x [SSM x KBP] K-major
   float* recv = reinterpret_cast<float*>(AS + MS * blk_bytes);          // global mode: [CL src][N][UPC]
-  float* recv1 = dsm ? recv + recv_bytes / 4 : recv;                    // DSMEM mode: 2 x [CL src][UPC][N]
-  uint8_t* dgB = reinterpret_cast<uint8_t*>(recv1) + recv_bytes;        // [N x KBP] K-major
+  float* recv1 = dsm ? recv + recv_span / 4 : recv;                     // DSMEM mode: 2 x [CL src][UPC][N]
+  uint8_t* dgB = reinterpret_cast<uint8_t*>(recv1) + recv_span;         // [N x KBP] K-major
   float* dbs = reinterpret_cast<float*>(dgB + N * KBP * 2);             // [NG][N][UPC] db scratch
   float* term = dbs + NG * N * a.UPC;                                    // DSMEM mode: [N][TP] summed R^T dg
   uint64_t* bars = reinterpret_cast<uint64_t*>(term + (dsm ? N * TP : 0));  // -, rcv, rdy0|rcv0, rdy1|rcv1
@@ -491,13 +566,15 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   // ---- element ownership: one pair (u, u+1) of one batch row b per thread
   const int NP = a.UPC / 2;
   const bool own = tid < NP * N;
-  const int u = 2 * (tid % NP), b = tid / NP;
+  int u, b;
+  own_pair(tid, NP, u, b);
   const bool valid = own && b < nb;
   const int e = hd * DH + unit0 + u;
   const size_t so = (size_t)(b0 + b) * D + e;       // [.][B][D]
   const size_t xo = (size_t)(b0 + b) * p.NG * D + e;  // [.][B][NG][D]
   const size_t sstep = (size_t)NS * B * D, gstep = (size_t)NG * B * D;
   float ds[NS][2], dbv[NG][2];
+  float kc[2][C::NK];  // Jacobian coefficients of the step about to be applied
   uint32_t pv[NS], gv[NG], hv = 0;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
@@ -512,17 +589,34 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     gv[j] = 0;
   }
   // Predicated loads (no select on the loaded value): issuing the prefetch
-  // never waits for it.
-  auto prefetch = [&](int t) {
+  // never waits for it.  The trace of step t is loaded two steps ahead: its
+  // Jacobian coefficients are formed during step t+1's MMA window.
+  auto load_trace = [&](int t) {
     if (valid && t >= 0) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) pv[s] = ld2(states, (size_t)t * sstep + (size_t)s * B * D + so);
 #pragma unroll
       for (int j = 0; j < NG; ++j) gv[j] = ld2(gates, (size_t)t * gstep + (size_t)j * B * D + so);
-      if (dh) hv = ld2(dh, (size_t)t * B * D + so);
     }
   };
-  prefetch(T - 1);
+  auto load_dh = [&](int t) {
+    if (valid && t >= 0 && dh) hv = ld2(dh, (size_t)t * B * D + so);
+  };
+  auto coefs = [&]() {  // kc <- Jacobian coefficients of the trace in pv/gv (cell.hpp:108-201)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float prev[4], g[4];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) prev[s] = h ? hi16(pv[s]) : lo16(pv[s]);
+#pragma unroll
+      for (int j = 0; j < NG; ++j) g[j] = h ? hi16(gv[j]) : lo16(gv[j]);
+      C::template coef<M>(prev, g, kc[h]);
+    }
+  };
+  load_trace(T - 1);
+  load_dh(T - 1);
+  if (T > 0) coefs();
+  load_trace(T - 2);
   __syncthreads();
   cluster_sync_all();  // barrier inits visible before any remote arrive
 
@@ -567,14 +661,54 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
     mbar_wait_cluster(&bars[2 + pb], (par_phase >> pb) & 1u);
     par_phase ^= 1u << pb;
-    if (own && pbf) {  // words [src][n/2][cu]: the (u, u+1) pair of words, half b&1 of each
-      const uint32_t* rp = reinterpret_cast<const uint32_t*>(pb ? recv1 : recv) + (size_t)(b >> 1) * a.UPC + u;
+    FRNN_PROF(5, T - 1 - (s - 1));
+    if (own && pbf && a.pvec == 2) {  // words [src][n][PW]: one word per source = units (u, u+1) of row b
+      const uint32_t* rp = reinterpret_cast<const uint32_t*>(pb ? recv1 : recv) + (size_t)b * PW + (u >> 1);
+      const size_t qs = (size_t)N * PW;
+      float t0 = 0.f, t1 = 0.f;
+      if (a.CL == 16) {  // all loads in flight first, then the fixed-order sums (deterministic)
+        uint32_t v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = rp[q * qs];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          t0 += lo16(v[q]);
+          t1 += hi16(v[q]);
+        }
+      } else {
+        for (int q = 0; q < a.CL; ++q) {
+          const uint32_t v = rp[q * qs];
+          t0 += lo16(v);
+          t1 += hi16(v);
+        }
+      }
+      if (p.clip_mode == 1) {
+        t0 = fminf(fmaxf(t0, -mag), mag);
+        t1 = fminf(fmaxf(t1, -mag), mag);
+      }
+      ds[0][0] += t0;
+      ds[0][1] += t1;
+    } else if (own && pbf) {  // words [src][u/2][b/2][2] (push_pair_cols) or [src][b/2][cu]: units (u, u+1), half b&1
+      const uint32_t* rp = reinterpret_cast<const uint32_t*>(pb ? recv1 : recv) +
+                           (a.pvec ? (size_t)(u >> 1) * N + (b >> 1) * 2 : (size_t)(b >> 1) * a.UPC + u);
       const size_t qs = (size_t)(N / 2) * a.UPC;
       float t0 = 0.f, t1 = 0.f;
-      for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
-        const uint2 v = *reinterpret_cast<const uint2*>(rp + q * qs);
-        t0 += (b & 1) ? hi16(v.x) : lo16(v.x);
-        t1 += (b & 1) ? hi16(v.y) : lo16(v.y);
+      const int sh = (b & 1) ? 0 : 16;  // lo16 = bits << 16, hi16 = bits & 0xffff0000
+      if (a.CL == 16 && a.absu) {  // all loads in flight first, then the fixed-order sums (deterministic)
+        uint2 v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = *reinterpret_cast<const uint2*>(rp + q * qs);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          t0 += __uint_as_float((v[q].x << sh) & 0xFFFF0000u);
+          t1 += __uint_as_float((v[q].y << sh) & 0xFFFF0000u);
+        }
+      } else {
+        for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
+          const uint2 v = *reinterpret_cast<const uint2*>(rp + q * qs);
+          t0 += (b & 1) ? hi16(v.x) : lo16(v.x);
+          t1 += (b & 1) ? hi16(v.y) : lo16(v.y);
+        }
       }
       if (p.clip_mode == 1) {
         t0 = fminf(fmaxf(t0, -mag), mag);
@@ -586,10 +720,21 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       const float* rp = (pb ? recv1 : recv) + (size_t)b * a.UPC + u;
       const size_t qs = (size_t)N * a.UPC;
       float t0 = 0.f, t1 = 0.f;
-      for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
-        const float2 v = *reinterpret_cast<const float2*>(rp + q * qs);
-        t0 += v.x;
-        t1 += v.y;
+      if (a.CL == 16 && a.absu) {  // all loads in flight first, then the fixed-order sums
+        float2 v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = *reinterpret_cast<const float2*>(rp + q * qs);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          t0 += v[q].x;
+          t1 += v[q].y;
+        }
+      } else {
+        for (int q = 0; q < a.CL; ++q) {  // fixed source order: deterministic
+          const float2 v = *reinterpret_cast<const float2*>(rp + q * qs);
+          t0 += v.x;
+          t1 += v.y;
+        }
       }
       if (p.clip_mode == 1) {
         t0 = fminf(fmaxf(t0, -mag), mag);
@@ -648,26 +793,33 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     if (recur && t + 1 < T) absorb(t + 1);
     FRNN_PROF(1, k);
     float dgv[NG][2];
+    // dx = dg for input-wired gates, engine.hpp:311-316 (off the critical path)
+    auto store_dx = [&]() {
+      if (valid) {
+        bf16* dxt = dx + (size_t)t * gstep + xo;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+          if (p.inp[j]) st2(dxt, (size_t)j * D, dgv[j][0], dgv[j][1]);
+          else *reinterpret_cast<uint32_t*>(dxt + (size_t)j * D) = 0u;
+          if (a.dgw) st2(a.dgw + (size_t)t * gstep + xo, (size_t)j * D, dgv[j][0], dgv[j][1]);
+        }
+      }
+    };
     if (own) {
       uint32_t pk[2][2] = {{0u, 0u}, {0u, 0u}};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        float prev[4], g[4], dsl[4], dg[4], dsp[4];
+        float dsl[4], dg[4], dsp[4];
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          prev[s] = h ? hi16(pv[s]) : lo16(pv[s]);
-          dsl[s] = ds[s][h];
-        }
+        for (int s = 0; s < NS; ++s) dsl[s] = ds[s][h];
         dsl[0] += h ? hi16(hv) : lo16(hv);  // engine.hpp:258-263
-#pragma unroll
-        for (int j = 0; j < NG; ++j) g[j] = h ? hi16(gv[j]) : lo16(gv[j]);
         if (a.skeleton) {
 #pragma unroll
-          for (int j = 0; j < NG; ++j) dg[j] = g[j] * dsl[0];
+          for (int j = 0; j < NG; ++j) dg[j] = dsl[0];
 #pragma unroll
           for (int s = 0; s < NS; ++s) dsp[s] = dsl[s];
         } else {
-          C::template bwd<M>(prev, g, dsl, dg, dsp);
+          C::apply(kc[h], dsl, dg, dsp);  // engine.hpp:275-284 with the coefficients formed last step
         }
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
@@ -687,7 +839,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       else
         *reinterpret_cast<uint32_t*>(dgB + kmaj(b, u, N)) = (pk[0][0] & 0xFFFFu) | (pk[1][0] << 16);
     }
-    prefetch(t - 1);
+    load_dh(t - 1);
     if (recur) {
       fence_proxy_async_smem();
       __syncthreads();
@@ -772,6 +924,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           __syncwarp();
         }
       }
+    }
+    // Under step t's MMAs: the Jacobian of step t-1 (its trace landed during step
+    // t+1), then the trace loads for step t-2.
+    if (t > 0 && !a.skeleton) coefs();
+    load_trace(t - 2);
+    if (a.dxearly) store_dx();
+    if (recur) {
       FRNN_PROF(3, k);
       // partial R_p^T dg_p, column c -> owner CTA c / UPC, layout [dest][src][b][u];
       // every warp drains the TMEM lane quadrant w%4 of blocks w/4, w/4+NT/128, ...
@@ -790,12 +949,17 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           mbar_wait(&blkbar[e ? i1 : i0], mma_phase);
+          FRNN_PROF_AT(6, k, NT - 32);  // the last warp's last block complete
           tc_fence_after();
           const int c = (e ? c1 : c0) + 32 * qd + l, q = c / 48, cu = c % 48;
           float v[16];
           tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (e ? a1 : a0) * N, v);
           const uint32_t mbr = mapa_shared(rbar, q);
-          if (pbf) {  // words [src][n/2][cu] = bf16 (n even, n odd)
+          if (pbf && a.pvec == 2) {
+            push_col_pairs<N>(v, l, true, cu, pair_pitch(48), rb + (uint32_t)(me * N * pair_pitch(48) * 4), q, mbr);
+          } else if (pbf && a.pvec) {
+            push_pair_cols<N>(v, l, true, cu, rb + (uint32_t)(me * (N / 2) * 48 * 4), q, mbr);
+          } else if (pbf) {  // words [src][n/2][cu] = bf16 (n even, n odd)
             const uint32_t dst = mapa_shared(rb + (uint32_t)((me * (N / 2) * 48 + cu) * 4), q);
 #pragma unroll
             for (int n2 = 0; n2 < N / 2; ++n2)
@@ -817,6 +981,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           sblk = MS > MBT;
         }
         mbar_wait(&blkbar[i], mma_phase);
+        FRNN_PROF_AT(6, k, NT - 32);  // the last warp's last block complete
         tc_fence_after();
         int c;
         bool lane_ok = true;
@@ -830,7 +995,15 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         }
         float v[16];
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (sblk ? MBT + i : i) * N, v);
-        if (lane_ok && c < DH) {
+        if (pbf && a.pvec == 2) {  // whole warp (shuffles inside)
+          const int q = min(c / a.UPC, a.CL - 1), cu = c % a.UPC;  // (clamped for lanes past DH)
+          push_col_pairs<N>(v, l, lane_ok && c < DH, cu, PW, rb + (uint32_t)(me * N * PW * 4), q,
+                            mapa_shared(rbar, q));
+        } else if (pbf && a.pvec) {  // whole warp (shuffles inside)
+          const int q = min(c / a.UPC, a.CL - 1), cu = c % a.UPC;  // (clamped for lanes past DH)
+          push_pair_cols<N>(v, l, lane_ok && c < DH, cu, rb + (uint32_t)(me * (N / 2) * a.UPC * 4), q,
+                            mapa_shared(rbar, q));
+        } else if (lane_ok && c < DH) {
           const bool u48 = a.UPC == 48;  // the H=768 tiling: constant divisor and stride
           const int q = u48 ? c / 48 : c / a.UPC, cu = u48 ? c % 48 : c % a.UPC;
           if (a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
@@ -863,6 +1036,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           }
         }
       }
+      FRNN_PROF_AT(7, k, NT - 32);  // the last warp's pushes issued
       mma_phase ^= 1;
       if (!dsm) fence_proxy_async_global();
       tc_fence_before();
@@ -870,16 +1044,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       if (!dsm && tid < a.CL) mbar_arrive_remote(mapa_shared(smem_u32(&bars[2 + (t & 1)]), tid));
       FRNN_PROF(4, k);
     }
-    // Off the critical path: dx (= dg for input-wired gates, engine.hpp:311-316).
-    if (valid) {
-      bf16* dxt = dx + (size_t)t * gstep + xo;
-#pragma unroll
-      for (int j = 0; j < NG; ++j) {
-        if (p.inp[j]) st2(dxt, (size_t)j * D, dgv[j][0], dgv[j][1]);
-        else *reinterpret_cast<uint32_t*>(dxt + (size_t)j * D) = 0u;
-        if (a.dgw) st2(a.dgw + (size_t)t * gstep + xo, (size_t)j * D, dgv[j][0], dgv[j][1]);
-      }
-    }
+    if (!a.dxearly) store_dx();
   }
   if (recur && T > 0) absorb(0);
   if (valid) {
@@ -1005,6 +1170,9 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   // bytes and pushes; backward 4.10 -> 3.58 us/step at H=768, gradient errors vs the
   // f64 oracle 1.75e-3 -> 1.82e-3 normwise); FRNN_PBF16=0/1 overrides.
   a.pbf16 = getenv("FRNN_PBF16") ? atoi(getenv("FRNN_PBF16")) : (p.NG == 4 ? 1 : 0);
+  a.dxearly = getenv("FRNN_DXEARLY") ? atoi(getenv("FRNN_DXEARLY")) : 0;
+  a.absu = getenv("FRNN_ABSU") ? atoi(getenv("FRNN_ABSU")) : 1;
+  a.pvec = getenv("FRNN_PVEC") ? atoi(getenv("FRNN_PVEC")) : 2;
   a.skeleton = g_skeleton;
   char* w = static_cast<char*>(ws);
   if (!backward) {

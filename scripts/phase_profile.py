@@ -39,6 +39,9 @@ s0 = (0.5 * torch.randn(NS, a.batch, a.hidden, device=dev, generator=g)).bfloat1
 dsf = torch.randn(NS, a.batch, a.hidden, device=dev, generator=g).bfloat16()
 eng = FlashRNN()
 L = load()
+if os.environ.get("FRNN_DEBUG_SKELETON"):  # synchronisation skeleton only (results are garbage)
+    L.frnn_debug_skeleton.argtypes = [C.c_int32]
+    L.frnn_debug_skeleton(1)
 L.frnn_debug_profile.argtypes = [C.c_void_p, C.c_int32]
 pf = eng.plan(a.variant, a.seq, a.batch, a.heads, DH, "bf16", "forward")
 pb = eng.plan(a.variant, a.seq, a.batch, a.heads, DH, "bf16", "backward")
@@ -48,7 +51,7 @@ eng.backward(a.variant, R, b, st, ga, dsf)
 torch.cuda.synchronize()
 
 
-def profile(name, grid, run, labels, extra=()):
+def profile(name, grid, run, labels, extra=(), cross=()):
     buf = torch.zeros(grid * a.seq * 8, dtype=torch.int64, device=dev)
     L.frnn_debug_profile(buf.data_ptr(), a.seq)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -76,6 +79,9 @@ def profile(name, grid, run, labels, extra=()):
     for lab, k0, k1 in extra:  # stamp k1 - stamp k0 of the same step (thread 0)
         q = sorted(v[c][t][k1] - v[c][t][k0] for c in range(grid) for t in range(lo, hi))
         print(f"   {lab:>26s}: {q[len(q) // 2]:8.0f} {q[len(q) // 10]:8.0f} {q[9 * len(q) // 10]:8.0f}   (median p10 p90)")
+    for lab, k0, k1 in cross:  # stamp k1 of step t+1 - stamp k0 of step t (same CTA)
+        q = sorted(v[c][t + 1][k1] - v[c][t][k0] for c in range(grid) for t in range(lo, hi))
+        print(f"   {lab:>26s}: {q[len(q) // 2]:8.0f} {q[len(q) // 10]:8.0f} {q[9 * len(q) // 10]:8.0f}   (median p10 p90)")
 
 
 profile("fwd", pf["grid"], lambda: eng.forward(a.variant, R, b, x, s0, st, ga),
@@ -83,4 +89,9 @@ profile("fwd", pf["grid"], lambda: eng.forward(a.variant, R, b, x, s0, st, ga),
          "loop"],
         [("  of which tmem->xs+sync", 2, 5), ("  of which cell math", 5, 6), ("  of which h slice+sync", 6, 3)])
 profile("bwd", pb["grid"], lambda: eng.backward(a.variant, R, b, st, ga, dsf),
-        ["absorb(wait+load+sum)", "jacobian", "mma", "partials out+arrive", "dx stores"])
+        ["absorb(wait+load+sum)", "jacobian", "mma", "partials out+arrive", "dx stores"],
+        [("  issue -> last block done", 2, 6), ("  last block drained+pushed", 6, 7),
+         ("  of absorb: sum+clip", 5, 1)],
+        # critical path across CTAs: last warp's pushes of step k (slot 7) -> the
+        # partials of step k complete at thread 0 of every CTA (slot 5 of step k+1)
+        [("  pushes -> arrival (same CTA)", 7, 5)])

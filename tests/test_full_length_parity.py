@@ -20,7 +20,10 @@ perturbed to the GPU trace's measured distance and rounded to bf16, against
 the same backward on the unrounded trace (max over realizations).  For
 Elman/LSTM/GRU the control is ~1e-3 and the bound stays at 2e-2; for sLSTM the stabiliser's max branch
 (cell.hpp:153, ties to the forget branch) flips at near-tie elements under
-any bf16-level trace change, and the control is what that costs.
+any bf16-level trace change, and the control is what that costs.  The sLSTM
+bound uses max(control, sensitivity), sensitivity = the oracle backward on the
+GPU's own bf16 trace vs on the f64 trace (which near-tie elements flip is
+specific to a trace; at T=1024 the control alone already covers it).
 Per-column slices guard against a localised error (one CTA, one head)
 hiding under a normwise figure: each 48-column slice must stay within
 SLICE_FACTOR x the tensor's bound.
@@ -129,6 +132,8 @@ def test_full_length_parity(eng, orc, cid, v, NH, step):
     for k in GRADS:
         rec["same_trace"][k] = stats(gpu[k], same[k], k)
         rec["end_to_end"][k] = stats(gpu[k], ora[k], k)
+        # the oracle's response to the GPU's own (forward-checked) bf16 trace
+        rec.setdefault("sensitivity", {})[k] = normwise(same[k], ora[k])
     # sLSTM: how many stabiliser branches the bf16 trace flips (cell.hpp:153)
     if v == "slstm":
         def branch(states, gates):
@@ -157,7 +162,7 @@ def test_full_length_parity(eng, orc, cid, v, NH, step):
         s = rec["same_trace"][k]
         if not s["normwise"] <= BF16_TOL or not s["worst_slice"] <= SLICE_FACTOR * BF16_TOL:
             bad.append(("same_trace", k, s))
-        bound = BF16_TOL + rec["control"][k] if v == "slstm" else BF16_TOL
+        bound = BF16_TOL + max(rec["control"][k], rec["sensitivity"][k]) if v == "slstm" else BF16_TOL
         s = rec["end_to_end"][k]
         if not s["normwise"] <= bound or not s["worst_slice"] <= SLICE_FACTOR * bound:
             bad.append(("end_to_end", k, bound, s))

@@ -19,7 +19,10 @@ Tolerances (stated here and in DESIGN.md section 6):
         perturbed to the GPU trace's measured distance and rounded to bf16, vs
         on the f64 trace, max over 8 realizations (the plain-rounding control
         is pinned on the CPU by tests/test_oracle.py::test_bf16_trace_control);
-        sLSTM end to end is bounded by 2e-2 + control per gradient.
+        sLSTM end to end is bounded by 2e-2 + max(control, sensitivity) per
+        gradient, where sensitivity = the oracle backward on the GPU's own
+        (forward-checked) bf16 trace vs on the f64 trace: at small T the random
+        realizations need not flip the same near-tie elements the GPU trace flips.
     Full-length (T=1024) versions of these checks: tests/test_full_length_parity.py.
 """
 import numpy as np
@@ -94,8 +97,13 @@ def check_bf16(eng, orc, v, inp, clip="off", mag=0.0, dh=None, algo="auto"):
         ctl, _ = trace_control(orc, v, r["R"], ora["states"], ora["gates"], r["dsf"],
                                fwd["states"], 8, clip, mag,
                                orc.round_bf16(dh) if dh is not None else None)
-        bad = {k: (e2e[k], ctl[k]) for k in GRADS if not e2e[k] <= BF16_TOL + ctl[k]}
-        assert not bad, ("sLSTM end to end above control + 2e-2", bad)
+        # the oracle's response to the exact bf16 trace the GPU produced (checked
+        # above): at small T the random realizations may flip other near-tie
+        # elements than the GPU trace does, so the bound takes the larger of the two
+        sens = {k: normwise(cond[k], ora[k]) for k in GRADS}
+        bad = {k: (e2e[k], ctl[k], sens[k]) for k in GRADS
+               if not e2e[k] <= BF16_TOL + max(ctl[k], sens[k])}
+        assert not bad, ("sLSTM end to end above max(control, trace sensitivity) + 2e-2", bad)
     else:
         assert max(e2e.values()) <= BF16_TOL, e2e
     print(v, "fwd", fwd, "bwd(same trace)", bwd, "e2e", e2e)
