@@ -66,5 +66,27 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+TOOLS = ("frnn", "e2e_bench")  # tools/<name>.cpp -> build/<name>: C++ callers of the drop-in header
+
+
+def build_tool(name: str) -> str:
+    """g++ a tools/<name>.cpp program against include/ and libflashrnn.so."""
+    exe = os.path.join(ROOT, "build", name)
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(cuda, "include"),
+           os.path.join(ROOT, "tools", name + ".cpp"), "-o", exe, "-L" + PKG, "-lflashrnn",
+           "-L" + os.path.join(cuda, "lib64"), "-lcudart", "-lpthread",
+           "-Wl,-rpath," + PKG + ":" + os.path.join(cuda, "lib64")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed for tools/{name}.cpp:\n{r.stderr}")
+    return exe
+
+
+def build_tools() -> list:
+    return [build_tool(n) for n in TOOLS]
+
+
 if __name__ == "__main__":
     print(build(verbose="--verbose" in sys.argv))
