@@ -55,7 +55,10 @@ def parse():
     ap.add_argument("--variant", default="slstm", choices=list(NS_NG))
     ap.add_argument("--heads", type=int, default=1)
     ap.add_argument("--hidden", type=int, default=768)
-    ap.add_argument("--batch", type=int, default=16, help="batch rows per GPU")
+    ap.add_argument("--batch", type=int, default=16,
+                    help="batch rows per GPU (weak scaling) or in total (strong scaling)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: B rows per GPU (global B = B x N); strong: global B fixed, sharded over the N GPUs")
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=64)
@@ -64,7 +67,8 @@ def parse():
 
 def workload_name(a, algo=None):
     path = {1: " (fused kernel, R resident on-chip)", 2: " (alternating path, R streamed from L2 every step)"}
-    return (f"{a.variant} fwd+bwd bf16, B={a.batch}/GPU, T={a.seq}, H={a.hidden}, NH={a.heads}"
+    bdesc = f"B={a.batch} total" if getattr(a, "scaling", "weak") == "strong" else f"B={a.batch}/GPU"
+    return (f"{a.variant} fwd+bwd bf16, {bdesc}, T={a.seq}, H={a.hidden}, NH={a.heads}"
             + path.get(algo, ""))
 
 
@@ -301,7 +305,21 @@ def run_ours(a, rank, world, local_rank):
     L.frnn_debug_timing.argtypes = [C.c_int32]
     L.frnn_debug_launches.argtypes = [C.POINTER(C.c_int64)]
     L.frnn_debug_kernel_ms.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
-    shard = partition(a.seq, a.batch * world, a.heads, a.hidden // a.heads, world, rank)
+    # the rank's (batch x head) shard of the global problem (frnn_partition); every
+    # kernel below runs on the LOCAL shape, the metric counts the global one
+    DH = a.hidden // a.heads
+    global_B = a.batch * world if a.scaling == "weak" else a.batch
+    shard = partition(a.seq, global_B, a.heads, DH, world, rank)
+    ga_ = argparse.Namespace(**vars(a))  # global view (names, FLOP accounting)
+    a = argparse.Namespace(**vars(a))
+    a.batch = shard["batch_end"] - shard["batch_begin"]
+    a.heads = shard["head_end"] - shard["head_begin"]
+    a.hidden = a.heads * DH
+    libdist = None
+    share = os.environ.get("FRNN_BENCH_SHARE_GPU") == "1"  # test hook: ranks share cuda:0 (gloo, no NCCL)
+    if world > 1 and not share:  # the library's own NCCL layer (include/flashrnn_dist.h); torch ships the NCCL id
+        from paper_2412_07752_b200.distributed import LibDist
+        libdist = LibDist(world, rank, bootstrap=dist)
     inp = make_inputs(torch, dev, a, seed=rank)
     ns, ng = NS_NG[a.variant]
     D = a.hidden
@@ -312,12 +330,17 @@ def run_ours(a, rank, world, local_rank):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    def reduce(o):  # dR/db summed over batch shards (engine.hpp:317, :327-330): the only collective
+        if libdist is not None:
+            libdist.reduce_param_grads(a.variant, a.seq, global_B, ga_.heads, DH, o["dR"], o["dbias"])
+        elif world > 1:  # FRNN_BENCH_SHARE_GPU test hook only
+            from paper_2412_07752_b200.distributed import reduce_param_grads
+            reduce_param_grads(o["dR"], o["dbias"], shard, dist, a.seq, global_B, ga_.heads, DH)
+
     def step():
         eng.forward(a.variant, inp["R"], inp["bias"], inp["x"], inp["s0"], st, ga)
         eng.backward(a.variant, inp["R"], inp["bias"], st, ga, inp["dsf"], out=out)
-        if world > 1:  # data-parallel parameter-gradient reduction (the only collective)
-            dist.all_reduce(out["dR"])
-            dist.all_reduce(out["dbias"])
+        reduce(out)
 
     for _ in range(a.warmup):
         step()
@@ -355,8 +378,33 @@ def run_ours(a, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = t.item()
     ms_step = total_ms / a.steps
-    units = a.batch * a.seq * world
+    units = global_B * a.seq
     value = units / (ms_step / 1e3)
+
+    # ---- the post-run gather of the sharded outputs, timed apart:
+    # states / gates / dx / ds0 / dR / db assembled at the global shape on every rank
+    gather = None
+    if libdist is not None:
+        cs = {"states": (a.seq + 1, ns, global_B, ga_.hidden), "gates": (a.seq, ng, global_B, ga_.hidden),
+              "dx": (a.seq, global_B, ng, ga_.hidden), "ds0": (ns, global_B, ga_.hidden),
+              "dR": (ga_.heads, ng, DH, DH), "dbias": (ng, ga_.hidden)}
+        local = {"states": st, "gates": ga, **out}
+        full = {k: torch.empty(v, dtype=torch.bfloat16, device=dev) for k, v in cs.items()}
+        libdist.gather(a.variant, a.seq, global_B, ga_.heads, DH, local, full)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(3):
+            libdist.gather(a.variant, a.seq, global_B, ga_.heads, DH, local, full)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = torch.tensor([g0.elapsed_time(g1) / 3], device=dev, dtype=torch.float64)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        gbytes = sum(v.numel() * 2 for v in full.values())
+        gather = {"ms": gms.item(), "bytes_per_rank_out": gbytes,
+                  "note": "frnn_dist_gather (ncclAllGather + placement), outside the timed step"}
+        del full
 
     # ---- roofline of the dominant kernel (live CUDA-event timing) ----
     plan = {p: eng.plan(a.variant, a.seq, a.batch, a.heads, a.hidden // a.heads, "bf16", p)
@@ -453,9 +501,7 @@ def run_ours(a, rank, world, local_rank):
         eng.forward(a.variant, d["R"], d["bias"], d["x"], d["s0"], o["st"], o["ga"])
         eng.backward(a.variant, d["R"], d["bias"], o["st"], o["ga"], d["dsf"],
                      out={k: o[k] for k in ("dx", "dbias", "dR", "ds0")})
-        if world > 1:
-            dist.all_reduce(o["dR"])
-            dist.all_reduce(o["dbias"])
+        reduce(o)
         freed[j].record(stream)
         done[j].record(stream)
         ostream.wait_event(done[j])
@@ -527,15 +573,18 @@ def run_ours(a, rank, world, local_rank):
         return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": a.scaling,
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (torch RNG on device, reference generator distributions)",
-        "config": {"workload": workload_name(a, plan["forward"]["algo"]), "variant": a.variant, "batch_per_gpu": a.batch,
-                   "global_batch": a.batch * world, "seq_len": a.seq, "hidden": a.hidden, "heads": a.heads,
-                   "parallelism": f"batch-shard x{world} (frnn_partition: {shard})" if world > 1 else "single GPU",
+        "config": {"workload": workload_name(ga_, plan["forward"]["algo"]), "variant": a.variant, "batch_per_gpu": a.batch,
+                   "global_batch": global_B, "seq_len": a.seq, "hidden": ga_.hidden, "heads": ga_.heads,
+                   "parallelism": (f"batch x head shards x{world} (frnn_partition, rank 0: {shard}); dR/db "
+                                   f"ncclAllReduce (fp32) in the step via libflashrnn's NCCL layer")
+                   if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MB write, outside the events)"},
         "roofline": roof,
         "e2e": e2e,
+        **({"gather": gather} if gather else {}),
         "gpu_launches": int(launches1.value - launches0.value),
         "clocks": clk,
         "plan": {k: {kk: v[kk] for kk in ("algo", "grid", "ctas_per_group", "units_per_cta", "tmem_cols",

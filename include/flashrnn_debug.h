@@ -31,6 +31,12 @@ FRNN_API int frnn_debug_skeleton(int32_t enable);
  * FRNN_ALGO_ALTERNATING) for a shape, in the text form of flashrnn_csp.h. */
 FRNN_API int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
                                  int32_t algo, char* out, size_t out_bytes);
+/* The placement half of frnn_dist_gather (flashrnn_dist.h) for a `world`-rank
+ * layout, from a caller-filled staging buffer [world][blk] (what ncclAllGather
+ * would deliver) into the full tensor k (0 states, 1 gates, 2 dx, 3 ds0, 4 dR,
+ * 5 dbias); *blk_out = blk (elements).  NULL stage/full: just report blk. */
+FRNN_API int frnn_debug_dist_place(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t world, int32_t k,
+                                   const void* stage, void* full, size_t* blk_out, void* stream);
 #ifdef __cplusplus
 }
 #endif

@@ -310,6 +310,11 @@ size_t elem(const frnn::Problem& p) { return p.bf16 ? 2 : 4; }
 
 }  // namespace
 
+namespace frnn {  // the thread-local error string, for the other C-ABI translation units (dist.cu)
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+void clear_error() { g_err.clear(); }
+}  // namespace frnn
+
 extern "C" {
 
 const char* frnn_version(void) { return "flashrnn-b200 0.1.0 (sm_100a, abi 1)"; }

@@ -41,6 +41,10 @@ struct Plan {
   double solve_us;
 };
 
+// C-ABI error string (abi.cpp), shared by every exported entry point.
+int set_error(int code, const std::string& msg);
+void clear_error();
+
 // Workspace carve-up helpers.
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

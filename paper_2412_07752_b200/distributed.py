@@ -88,12 +88,121 @@ def gather_outputs(local: dict, s: dict, world: int, T: int, B: int, NH: int, DH
     return out
 
 
-def reduce_param_grads(dR, dbias, s: dict, dist) -> None:
-    """In-place data-parallel reduction used when every rank holds all heads
-    (pure batch sharding, the benchmark's weak-scaling layout)."""
-    if s["reduce_params"] and s["head_begin"] == 0:
+def reduce_param_grads(dR, dbias, s: dict, dist, T=None, B=None, NH=None, DH=None) -> None:
+    """In-place sum of dR / dbias over the ranks that share this rank's head
+    range (the batch shards; engine.hpp:317, :327-330).  With mixed head x
+    batch sharding every rank joins one torch.distributed subgroup per head
+    partition (new_group is collective, so all ranks create all groups in the
+    same order); pure batch sharding reduces over the whole world."""
+    if not s["reduce_params"]:
+        return
+    world = dist.get_world_size()
+    if NH is None:  # legacy call: only valid for pure batch sharding
+        if s["head_begin"] != 0:
+            raise ValueError("mixed head x batch sharding: pass T, B, NH, DH")
         dist.all_reduce(dR)
         dist.all_reduce(dbias)
+        return
+    shards = [shard_of(T, B, NH, DH, world, r) for r in range(world)]
+    heads = sorted({(x["head_begin"], x["head_end"]) for x in shards})
+    if len(heads) == 1:
+        dist.all_reduce(dR)
+        dist.all_reduce(dbias)
+        return
+    mine = None
+    for hb in heads:  # every rank creates every group, in the same order
+        g = dist.new_group([r for r, x in enumerate(shards) if (x["head_begin"], x["head_end"]) == hb])
+        if hb == (s["head_begin"], s["head_end"]):
+            mine = g
+    dist.all_reduce(dR, group=mine)
+    dist.all_reduce(dbias, group=mine)
+
+
+class LibDist:
+    """The library's own multi-GPU layer (include/flashrnn_dist.h): an NCCL
+    communicator created by libflashrnn (dlopen'ed NCCL, no PyTorch on its
+    data path), the fp32 dR/db reduction across batch shards and the
+    activation gather.  `bootstrap` only ships the 128-byte NCCL unique id from
+    rank 0 to the others (any torch.distributed process group will do)."""
+
+    def __init__(self, world: int, rank: int, bootstrap=None):
+        import ctypes as C
+
+        import torch
+
+        from .abi import load
+
+        self.C, self.torch = C, torch
+        self.world, self.rank = world, rank
+        L = self.lib = load()
+        vp = C.c_void_p
+        L.frnn_dist_unique_id.argtypes = [C.c_char_p]
+        L.frnn_dist_init.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(vp)]
+        L.frnn_dist_destroy.argtypes = [vp]
+        from .abi import Cell
+        pc = C.POINTER(Cell)
+        L.frnn_dist_workspace_size.argtypes = [vp, pc, _Shape(), C.c_int32, C.POINTER(C.c_size_t)]
+        L.frnn_dist_reduce_param_grads.argtypes = [vp, pc, _Shape(), C.c_int32, vp, vp, vp, C.c_size_t, vp]
+        L.frnn_dist_gather.argtypes = [vp, pc, _Shape(), C.c_int32, vp, vp, C.c_size_t, vp]
+        idb = C.create_string_buffer(128)
+        if rank == 0:
+            _chk(L.frnn_dist_unique_id(idb))
+        if world > 1:
+            t = torch.tensor(list(idb.raw), dtype=torch.uint8)
+            if bootstrap is not None and bootstrap.get_backend() == "nccl":
+                t = t.cuda()
+            bootstrap.broadcast(t, src=0)
+            idb = C.create_string_buffer(bytes(t.cpu().tolist()), 128)
+        self.handle = vp()
+        _chk(L.frnn_dist_init(idb, world, rank, C.byref(self.handle)))
+        self._ws = None
+
+    def _workspace(self, cell, shape, dt, device):
+        n = self.C.c_size_t()
+        _chk(self.lib.frnn_dist_workspace_size(self.handle, self.C.byref(cell), shape, dt, self.C.byref(n)))
+        if self._ws is None or self._ws.numel() < n.value:
+            self._ws = self.torch.empty(max(256, n.value), dtype=self.torch.uint8, device=device)
+        return self._ws
+
+    def reduce_param_grads(self, variant, T, B, NH, DH, dR, dbias, stream=None):
+        from .abi import DTYPE, Shape, cell_spec
+        cell, shape = cell_spec(variant), Shape(T, B, NH, DH)
+        dt = DTYPE["bf16"] if dR.dtype == self.torch.bfloat16 else DTYPE["f32"]
+        ws = self._workspace(cell, shape, dt, dR.device)
+        s = stream if stream is not None else self.torch.cuda.current_stream(dR.device).cuda_stream
+        _chk(self.lib.frnn_dist_reduce_param_grads(self.handle, self.C.byref(cell), shape, dt, dR.data_ptr(),
+                                                   dbias.data_ptr(), ws.data_ptr(), ws.numel(), s))
+
+    def gather(self, variant, T, B, NH, DH, local: dict, full: dict, stream=None):
+        """local/full: dicts with any of states, gates, dx, ds0, dR, dbias."""
+        from .abi import DTYPE, Shape, cell_spec
+        C = self.C
+        names = ("states", "gates", "dx", "ds0", "dR", "dbias")
+        ptr = [local[k].data_ptr() if k in local and k in full else None for k in names]
+        fptr = [full[k].data_ptr() if k in local and k in full else None for k in names]
+        tens = (C.c_void_p * 12)(*(ptr + fptr))
+        cell, shape = cell_spec(variant), Shape(T, B, NH, DH)
+        t0 = next(v for v in local.values())
+        dt = DTYPE["bf16"] if t0.dtype == self.torch.bfloat16 else DTYPE["f32"]
+        ws = self._workspace(cell, shape, dt, t0.device)
+        s = stream if stream is not None else self.torch.cuda.current_stream(t0.device).cuda_stream
+        _chk(self.lib.frnn_dist_gather(self.handle, C.byref(cell), shape, dt, C.cast(tens, C.c_void_p),
+                                       ws.data_ptr(), ws.numel(), s))
+
+    def close(self):
+        if self.handle:
+            self.lib.frnn_dist_destroy(self.handle)
+            self.handle = self.C.c_void_p()
+
+
+def _Shape():
+    from .abi import Shape
+    return Shape
+
+
+def _chk(rc):
+    from .abi import _check
+    _check(rc)
 
 
 def _all_gather_var(t, dist, world):
