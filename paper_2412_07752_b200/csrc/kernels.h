@@ -46,7 +46,7 @@ int set_error(int code, const std::string& msg);
 void clear_error();
 
 // Workspace carve-up helpers.
-inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+__host__ __device__ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // ---- SIMT fp32 path (simt_fp32.cu) ----
 size_t simt_smem_bytes(const Problem& p, bool backward);
@@ -66,6 +66,7 @@ struct ClusterShape {
   int UPC, CL, R1, R2, K, KBP, MB, MBT, EPT, groups, threads;
   int MS, SSM;  // backward: SMEM-A column blocks and their M (64 | 128)
   int dsm;  // backward partial exchange: 0 global + TMA bulk load, 1 DSMEM v4 [cu][n], 2 DSMEM rows [n][cu]
+  int pbf16, pvec;  // backward: bf16-pair partials; their receive layout (2 = [n][cu/2] column pairs)
   uint32_t acc1, acc2, tmem_cols, slice;
   size_t smem, ws;
 };

@@ -656,14 +656,39 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+__device__ __forceinline__ bool mbar_test_relaxed_cluster(uint32_t a, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.relaxed.cluster.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 "
+      "%0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void fence_acquire_cluster() { asm volatile("fence.acquire.cluster;" ::: "memory"); }
 // Wait on a local mbarrier whose arrivals/transactions come from other CTAs.
+// An acquire.cluster probe compiles to PHASECHK + CCTL.IVALL (an L1 invalidate)
+// on EVERY poll, which stalls the waiting warps' in-flight loads and those of
+// the warps beside them; the spin uses relaxed probes and acquires once
+// (fence.acquire.cluster) after the phase is observed complete.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
+#ifdef FRNN_ACQ_SPIN  // A/B build: acquire on every probe (round-1 protocol)
   if (mbar_try_cluster(a, phase)) return;
   const uint64_t t0 = globaltimer_ns();
   uint32_t n = 0;
   while (!(g_spin_wait ? mbar_test_cluster(a, phase) : mbar_try_cluster_sleep(a, phase, 1000000u)))
     if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
+#else
+  if (!mbar_test_relaxed_cluster(a, phase)) {
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
+    while (!mbar_test_relaxed_cluster(a, phase))
+      if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
+  }
+  fence_acquire_cluster();
+#endif
 }
 // Arrive (count 1) on the mbarrier at cluster-shared address `remote`.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t remote) {
@@ -721,6 +746,35 @@ __device__ __forceinline__ void tma_load_5d(void* smem, const void* map, int c0,
       "%6}], [%7];" ::"r"(smem_u32(smem)),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem, const void* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// TMA stores (smem -> global, bulk-group completion; out-of-bounds box rows are clipped).
+__device__ __forceinline__ void tma_store_3d(const void* map, int c0, int c1, int c2, const void* smem) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const void* map, int c0, int c1, int c2, int c3, const void* smem) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(smem))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until at most N committed bulk groups still READ their shared-memory source.
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// Wait until at most N committed bulk groups are incomplete (writes performed).
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void prefetch_tensormap(const void* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
