@@ -68,6 +68,7 @@ struct CArgs {
   int prof_steps;
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
+  int rot;         // backward column rotation per CTA (FRNN_ROT=1; A/B knob, off: no gain measured)
   int nodx, noload;  // debug (FRNN_DBG_NODX / FRNN_DBG_NOLOAD): skip the backward's dx stores / trace loads
   int noxchg;      // debug (FRNN_DBG_NOXCHG): backward without the partial exchange (results garbage)
   int dxearly;     // store dx inside the MMA window (after the Jacobian) -- A/B knob FRNN_DXEARLY
@@ -530,6 +531,12 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   uint64_t* blkbar = bars + 4;  // [NPAIR]: MMAs of block pair i (and all before it) complete
   uint32_t* tbase_s = reinterpret_cast<uint32_t*>(blkbar + 16);
 
+  // Column rotation: CTA `me` lays out its R^T column blocks starting at column
+  // me*UPC, so the block it computes LAST (whose partials arrive after the MMAs)
+  // belongs to different owners in every CTA.  Unrotated, all 16 CTAs' last
+  // blocks hit the same 3 owners, whose DSMEM ingress then serialises the tail.
+  const int crot = a.rot ? (int)(((long long)me * a.UPC) % DH) : 0;
+  auto rotc = [&](int c) { return c < DH ? (c + crot) % DH : c; };  // padding columns stay padding
   if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -544,7 +551,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     for (int ib = 0; ib < MS; ++ib) {
       uint8_t* blk = AS + ib * blk_bytes;
       for (int i = tid; i < SSM * KBP; i += NT) {
-        const int m = i % SSM, k = i / SSM, c = MBT * 128 + ib * SSM + m, uu = k / NGP, g = k % NGP;
+        const int m = i % SSM, k = i / SSM, c = rotc(MBT * 128 + ib * SSM + m), uu = k / NGP, g = k % NGP;
         const float v = (c < DH && uu < a.UPC && g < NG && p.rec[g])
                             ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
         *reinterpret_cast<bf16*>(blk + kmaj(m, k, SSM)) = __float2bfloat16_rn(v);
@@ -557,7 +564,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const uint32_t tbase = __shfl_sync(0xffffffffu, *tbase_s, 0);
   if (recur && w < 4) {  // R_slice^T blocks in TMEM: lane = state column, columns = row pairs
     for (int mb = 0; mb < MBT; ++mb) {
-      const int c = mb * 128 + 32 * w + l;
+      const int c = rotc(mb * 128 + 32 * w + l);
       for (int c0 = 0; c0 < KBP / 2; c0 += 16) {
         uint32_t v[16];
 #pragma unroll
@@ -967,7 +974,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           mbar_wait(&blkbar[e ? i1 : i0], mma_phase);
           FRNN_PROF_AT(6, k, NT - 32);  // the last warp's last block complete
           tc_fence_after();
-          const int c = (e ? c1 : c0) + 32 * qd + l, q = c / 48, cu = c % 48;
+          const int c = rotc((e ? c1 : c0) + 32 * qd + l), q = c / 48, cu = c % 48;
           float v[16];
           tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (e ? a1 : a0) * N, v);
           const uint32_t mbr = mapa_shared(rbar, q);
@@ -1009,6 +1016,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         } else {
           c = MBT * 128 + i * 128 + 32 * qd + l;
         }
+        c = rotc(c);
         float v[16];
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (sblk ? MBT + i : i) * N, v);
         if (FX || (pbf && a.pvec == 2)) {  // whole warp (shuffles inside)
@@ -1211,6 +1219,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.pvec = backward ? cs.pvec : 0;
 
   a.skeleton = g_skeleton || (getenv("FRNN_DBG_SKELETON") && atoi(getenv("FRNN_DBG_SKELETON")));
+  a.rot = getenv("FRNN_ROT") ? atoi(getenv("FRNN_ROT")) : 0;  // measured neutral-to-slower (DESIGN 8c)
   a.noxchg = backward && getenv("FRNN_DBG_NOXCHG") && atoi(getenv("FRNN_DBG_NOXCHG"));
   a.nodx = getenv("FRNN_DBG_NODX") && atoi(getenv("FRNN_DBG_NODX"));        // fwd: trace stores
   a.noload = getenv("FRNN_DBG_NOLOAD") && atoi(getenv("FRNN_DBG_NOLOAD"));  // fwd: x loads
