@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "kernels.h"
@@ -28,6 +29,10 @@ constexpr uint32_t CHUNK = 64 * 64 * 2;  // one [64 k][64 mn] swizzled box = 8 K
 
 struct GArgs {
   int NG, DH, NH, B, numk, BN;
+  // K tiling over k = (t, b): B <= 64: ksteps whole steps per tile (kreal = ksteps*B
+  // rows, the rest of the 64-row B tile stays zero); B > 64: one step, 64-row
+  // batch chunks (bchunks per step; rows past B are zero-filled by TMA)
+  int ksteps, bchunks, kreal;
   bool rec[4];
   bf16* dR;
 };
@@ -58,7 +63,7 @@ __global__ void __launch_bounds__(128, 1) dr_gemm_kernel(const __grid_constant__
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int BN = g.BN;
-  const uint32_t stage_bytes = 2 * CHUNK + (BN / 64) * CHUNK;
+  const uint32_t stage_bytes = 2 * CHUNK + (BN / 64) * CHUNK;  // (B tiles keep a full 64-row chunk)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
@@ -75,10 +80,20 @@ __global__ void __launch_bounds__(128, 1) dr_gemm_kernel(const __grid_constant__
     mbar_init(done, 1);
     fence_mbar_init();
   }
+  if (g.kreal < BK) {  // B tile rows kreal..63 are never written by TMA: zero them once
+    for (int s = 0; s < STAGES; ++s)
+      for (int q = 0; q < BN / 64; ++q) {
+        uint8_t* sb = smem + s * stage_bytes + 2 * CHUNK + q * CHUNK;
+        for (int i = g.kreal * 128 / 16 + tid; i < (int)(CHUNK / 16); i += blockDim.x)
+          reinterpret_cast<uint4*>(sb)[i] = make_uint4(0, 0, 0, 0);
+      }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, *tbase_s, 0);
+  const uint32_t b_box_bytes = (uint32_t)(g.B <= 64 ? g.B * g.ksteps : 64) * 128;  // one 64-column chunk
 
   if (w == 0) {  // TMA producer
     if (elect_one()) {
@@ -87,15 +102,17 @@ __global__ void __launch_bounds__(128, 1) dr_gemm_kernel(const __grid_constant__
         if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * stage_bytes;
         uint8_t* sb = sa + 2 * CHUNK;
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
+        mbar_arrive_expect_tx(&full[s], 2 * CHUNK + (BN / 64) * b_box_bytes);
+        // this tile's first (t, b): A rows past the tile's real k meet zero B rows
+        const int t0 = g.B <= 64 ? kt * g.ksteps : kt / g.bchunks;
+        const int bb0 = g.B <= 64 ? 0 : (kt % g.bchunks) * 64;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int m = m0 + 64 * h;  // 64 rows of one gate (DH % 64 == 0)
-          tma_load4(sa + h * CHUNK, &map_a, m % g.DH, hd, m / g.DH, kt * BK, &full[s]);
+          tma_load4(sa + h * CHUNK, &map_a, m % g.DH, hd, m / g.DH, t0 * g.B + bb0, &full[s]);
         }
-        // k = (t, b): a box spans BK/B consecutive steps x all B rows
         for (int q = 0; q < BN / 64; ++q)
-          tma_load4(sb + q * CHUNK, &map_b, n0 + 64 * q, hd, 0, kt * (BK / g.B), &full[s]);
+          tma_load4(sb + q * CHUNK, &map_b, n0 + 64 * q, hd, bb0, t0, &full[s]);
       }
     }
     __syncwarp();
@@ -178,7 +195,7 @@ int pick_bn(int DH) {
 }  // namespace
 
 bool dr_gemm_supported(const Problem& p) {
-  return p.bf16 && p.DH % 64 == 0 && p.B <= 64 && (64 % p.B) == 0 && (p.NG * p.DH) % BM == 0 && encoder() != nullptr;
+  return p.bf16 && p.DH % 64 == 0 && (p.NG * p.DH) % BM == 0 && encoder() != nullptr;
 }
 
 // dg: the dx-layout gate-gradient trace [T][B][NG][D] (dx, or the dgw
@@ -201,7 +218,7 @@ cudaError_t dr_gemm(const Problem& p, const void* dg, cudaStream_t s) {
   {  // B = h_t = states[t][0]: dims (c, head, b, t); one box = BK/B steps x B rows
     cuuint64_t dims[4] = {(cuuint64_t)p.DH, (cuuint64_t)p.NH, (cuuint64_t)p.B, (cuuint64_t)p.T};
     cuuint64_t strides[3] = {(cuuint64_t)p.DH * 2, (cuuint64_t)p.D * 2, (cuuint64_t)p.NS * p.B * p.D * 2};
-    cuuint32_t box[4] = {64, 1, (cuuint32_t)p.B, (cuuint32_t)(BK / p.B)};
+    cuuint32_t box[4] = {64, 1, (cuuint32_t)std::min(p.B, BK), (cuuint32_t)(p.B <= BK ? BK / p.B : 1)};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p.cstates), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -214,7 +231,10 @@ cudaError_t dr_gemm(const Problem& p, const void* dg, cudaStream_t s) {
   g.NH = p.NH;
   g.B = p.B;
   g.BN = BN;
-  g.numk = (int)(((long long)p.T * p.B + BK - 1) / BK);
+  g.ksteps = p.B <= BK ? BK / p.B : 1;
+  g.bchunks = p.B <= BK ? 1 : (p.B + BK - 1) / BK;
+  g.kreal = p.B <= BK ? g.ksteps * p.B : BK;
+  g.numk = p.B <= BK ? (p.T + g.ksteps - 1) / g.ksteps : p.T * g.bchunks;
   for (int j = 0; j < 4; ++j) g.rec[j] = p.rec[j];
   g.dR = static_cast<bf16*>(p.dR);
   const uint32_t stage_bytes = 2 * CHUNK + (BN / 64) * CHUNK;

@@ -200,6 +200,20 @@ def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
     check_bf16(eng, orc, v, inp)
 
 
+@pytest.mark.parametrize("B", [5, 24, 40, 48, 96, 130])
+def test_bf16_dr_gemm_any_batch(eng, orc, B):
+    """dR / db through the tcgen05 dR GEMM (dr_gemm.cu) at batch sizes that do
+    not divide its 64-deep K tile (engine.hpp:321-334 summed over t and b):
+    whole steps per tile for B <= 64 (zero-padded K rows), 64-row batch chunks
+    for B > 64.  Same-trace check against the oracle backward."""
+    v, T, NH, DH = "lstm", 7, 1, 128
+    inp = {k: orc.round_bf16(a) for k, a in orc.generate(v, T, B, NH, DH, seed=B).items()}
+    gpu = run_gpu(eng, v, inp, True)
+    cond = orc.backward(v, inp["R"], gpu["states"], gpu["gates"], inp["dsf"])
+    errs = assert_close(gpu, cond, BF16_TOL, ("dR", "dbias", "dx"))
+    print("B", B, errs)
+
+
 @pytest.mark.parametrize("pbf16", ["0", "1"])
 def test_bf16_partial_exchange_modes(eng, orc, monkeypatch, pbf16):
     """The backward's R^T.dg partials as fp32 (FRNN_PBF16=0) or bf16 pairs (the
