@@ -68,6 +68,8 @@ struct CArgs {
   int prof_steps;
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
+  int xpf;         // forward: L2 prefetch of x two steps ahead (FRNN_XPF)
+  int hdirect;     // forward: cell threads write h straight to the global staging slice (FRNN_HDIRECT)
   int rot;         // backward column rotation per CTA (FRNN_ROT=1; A/B knob, off: no gain measured)
   int nodx, noload;  // debug (FRNN_DBG_NODX / FRNN_DBG_NOLOAD): skip the backward's dx stores / trace loads
   int noxchg;      // debug (FRNN_DBG_NOXCHG): backward without the partial exchange (results garbage)
@@ -352,6 +354,14 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         for (int j = 0; j < NG; ++j)
           if (p.inp[j]) xn[j] = ld2(xp, (size_t)j * D);
       }
+      // x two steps ahead into L2 (no registers): next step's register loads then
+      // wait for L2, not HBM (one prefetch per 32-byte sector of a row)
+      if (a.xpf && t + 2 < T && (u & 15) == 0) {
+        const bf16* xq = x + (size_t)(t + 2) * gstep + xo;
+#pragma unroll
+        for (int j = 0; j < NG; ++j)
+          if (p.inp[j]) prefetch_l2(xq + (size_t)j * D);
+      }
     }
     mbar_wait(&bars[0], t & 1);
     tc_fence_after();
@@ -411,18 +421,26 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         for (int s = 0; s < NS; ++s) st[s][h] = nout[s][h] = nx[s];
       }
       FRNN_PROF(6, t);
-      *reinterpret_cast<uint32_t*>(hs + kmaj(b, u, N)) =
-          b < nb ? pack_bf16(nout[0][0], nout[0][1]) : 0u;  // padding rows stay zero
+      const uint32_t hword = b < nb ? pack_bf16(nout[0][0], nout[0][1]) : 0u;  // padding rows stay zero
+      if (a.hdirect && t + 1 < T) {  // straight into the global staging slice (the multicast source)
+        uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + ((t + 1) & 1)) * a.CL + me) * a.slice;
+        *reinterpret_cast<uint32_t*>(gst + kmaj(b, u, N)) = hword;
+        fence_proxy_async_global();  // this writer's generic store -> the multicast's async-proxy read
+      } else {
+        *reinterpret_cast<uint32_t*>(hs + kmaj(b, u, N)) = hword;
+      }
     }
     __syncthreads();
     FRNN_PROF(3, t);
     if (t + 1 < T) {  // publish h_{t+1}: slice -> global staging -> multicast to the cluster
       const int nbuf = (t + 1) & 1;
       uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + nbuf) * a.CL + me) * a.slice;
-      for (int i = tid; i < (int)(a.slice / 16); i += NT)
-        reinterpret_cast<uint4*>(gst)[i] = reinterpret_cast<const uint4*>(hs)[i];
-      if (tid < (int)(a.slice / 16)) fence_proxy_async_global();  // the writers' generic -> async proxy order
-      __syncthreads();
+      if (!a.hdirect) {
+        for (int i = tid; i < (int)(a.slice / 16); i += NT)
+          reinterpret_cast<uint4*>(gst)[i] = reinterpret_cast<const uint4*>(hs)[i];
+        if (tid < (int)(a.slice / 16)) fence_proxy_async_global();  // the writers' generic -> async proxy order
+        __syncthreads();
+      }
       FRNN_PROF(7, t);
       if (tid == 0) {
         mbar_arrive_expect_tx(&bars[1 + buf], (uint32_t)a.CL * a.slice);  // re-arm for step t+2
@@ -1219,6 +1237,8 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.pvec = backward ? cs.pvec : 0;
 
   a.skeleton = g_skeleton || (getenv("FRNN_DBG_SKELETON") && atoi(getenv("FRNN_DBG_SKELETON")));
+  a.hdirect = getenv("FRNN_HDIRECT") ? atoi(getenv("FRNN_HDIRECT")) : 1;  // fwd 2.52 -> 2.44 us/step
+  a.xpf = getenv("FRNN_XPF") ? atoi(getenv("FRNN_XPF")) : 0;
   a.rot = getenv("FRNN_ROT") ? atoi(getenv("FRNN_ROT")) : 0;  // measured neutral-to-slower (DESIGN 8c)
   a.noxchg = backward && getenv("FRNN_DBG_NOXCHG") && atoi(getenv("FRNN_DBG_NOXCHG"));
   a.nodx = getenv("FRNN_DBG_NODX") && atoi(getenv("FRNN_DBG_NODX"));        // fwd: trace stores
