@@ -69,6 +69,8 @@ struct CArgs {
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
   int xpf;         // forward: L2 prefetch of x two steps ahead (FRNN_XPF)
+  int csplit;      // backward: Jacobian coefficients under the previous MMA window (FRNN_COEFSPLIT)
+  int map;         // element ownership (own_pair): 1 = row-fastest groups of 8, 0 = unit-fastest
   int hdirect;     // forward: cell threads write h straight to the global staging slice (FRNN_HDIRECT)
   int rot;         // backward column rotation per CTA (FRNN_ROT=1; A/B knob, off: no gain measured)
   int nodx, noload;  // debug (FRNN_DBG_NODX / FRNN_DBG_NOLOAD): skip the backward's dx stores / trace loads
@@ -101,9 +103,16 @@ __device__ __forceinline__ void st2(bf16* p, size_t i, float lo, float hi) {
 // their 16-byte (backward dg) / 4-byte (forward h) stores into a K-major tile
 // land in the eight distinct 16-byte rows of one core matrix: no bank conflicts.
 // (Trace/x loads of a warp then touch 8 rows x 16 B -- off the critical path.)
-__device__ __forceinline__ void own_pair(int tid, int NP, int& u, int& b) {
-  u = 2 * ((tid >> 3) % NP);
-  b = (tid & 7) + 8 * (tid / (8 * NP));
+// map 0 (round 1): consecutive threads take consecutive unit pairs of one row
+// (coalesced trace / x / dx rows, but 8-way conflicted 16-byte dg-tile stores).
+__device__ __forceinline__ void own_pair(int tid, int NP, int& u, int& b, int map = 1) {
+  if (map) {
+    u = 2 * ((tid >> 3) % NP);
+    b = (tid & 7) + 8 * (tid / (8 * NP));
+  } else {
+    u = 2 * (tid % NP);
+    b = tid / NP;
+  }
 }
 
 // Backward partial exchange, bf16 pairs.  The receive block of source CTA `me`
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   const int NP = a.UPC / 2;
   const bool own = tid < NP * N;
   int u, b;
-  own_pair(tid, NP, u, b);
+  own_pair(tid, NP, u, b, a.map);
   const bool valid = own && b < nb;
   const int e = hd * DH + unit0 + u;
   const size_t so = (size_t)(b0 + b) * D + e;       // offset in [.][B][D] tensors
@@ -524,6 +533,15 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   // fraction of the generic kernel's code (i-cache: the generic instantiation is
   // ~16 k SASS instructions).
   constexpr bool FX = L == 1;
+  // L >= 1 (lean): only the default exchange (DSMEM row pushes; bf16 column pairs
+  // for 4-gate cells; unrolled absorb) is compiled in -- the A/B variants of the
+  // generic L = 0 instance cost the other tilings up to 25 % through code
+  // generation alone (same runtime path, measured)
+  constexpr bool LEAN = L >= 1;
+  // L == 3: lean, and no coefficient split, A/B or debug switch compiled in
+  constexpr bool RAW = L == 3;
+  const bool k_noxchg = !RAW && a.noxchg, k_nodx = !RAW && a.nodx, k_noload = !RAW && a.noload;
+  const bool dxearly = !RAW && a.dxearly;
   const bool pbf = FX || (a.pbf16 && a.dsm == 2);  // partials exchanged as bf16 pairs
   const int PW = pair_pitch(a.UPC);        // pvec 2 receive row pitch (words)
   const uint32_t recv_bytes = (uint32_t)a.CL * N * a.UPC * (pbf ? 2 : 4);  // exchanged bytes (expect_tx)
@@ -532,7 +550,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const size_t blk_bytes = (size_t)SSM * KBP * 2;  // one SMEM-A block
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  const bool dsm = FX || a.dsm != 0;
+  const bool dsm = LEAN || a.dsm != 0;
   const int TP = a.UPC + 2;                                              // term pitch (bank spread)
   uint8_t* AS = smem;                                                    // MS x [SSM x KBP] K-major
   float* recv = reinterpret_cast<float*>(AS + MS * blk_bytes);          // global mode: [CL src][N][UPC]
@@ -553,7 +571,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   // me*UPC, so the block it computes LAST (whose partials arrive after the MMAs)
   // belongs to different owners in every CTA.  Unrotated, all 16 CTAs' last
   // blocks hit the same 3 owners, whose DSMEM ingress then serialises the tail.
-  const int crot = a.rot ? (int)(((long long)me * a.UPC) % DH) : 0;
+  const int crot = (!RAW && a.rot) ? (int)(((long long)me * a.UPC) % DH) : 0;
   auto rotc = [&](int c) { return c < DH ? (c + crot) % DH : c; };  // padding columns stay padding
   if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
   if (tid == 0) {
@@ -606,7 +624,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const int NP = a.UPC / 2;
   const bool own = tid < NP * N;
   int u, b;
-  own_pair(tid, NP, u, b);
+  own_pair(tid, NP, u, b, a.map);
   const bool valid = own && b < nb;
   const int e = hd * DH + unit0 + u;
   const size_t so = (size_t)(b0 + b) * D + e;       // [.][B][D]
@@ -631,7 +649,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   // never waits for it.  The trace of step t is loaded two steps ahead: its
   // Jacobian coefficients are formed during step t+1's MMA window.
   auto load_trace = [&](int t) {
-    if (valid && t >= 0 && !a.noload) {
+    if (valid && t >= 0 && !k_noload) {
 #pragma unroll
       for (int s = 0; s < NS; ++s) pv[s] = ld2(states, (size_t)t * sstep + (size_t)s * B * D + so);
 #pragma unroll
@@ -654,8 +672,14 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   };
   load_trace(T - 1);
   load_dh(T - 1);
-  if (T > 0) coefs();
-  load_trace(T - 2);
+  // csplit: the coefficients of step t-1 are formed under step t's MMAs (trace
+  // loaded two steps ahead); otherwise (short MMA windows, where the extra MUFU
+  // work competes with the MMA-issuing warp) right before they are applied.
+  const bool csplit = !RAW && a.csplit != 0;
+  if (csplit) {
+    if (T > 0) coefs();
+    load_trace(T - 2);
+  }
   __syncthreads();
   cluster_sync_all();  // barrier inits visible before any remote arrive
 
@@ -697,13 +721,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   };
   auto absorb_rows = [&](int s) {  // DSMEM mode 2: recv[s&1] is [src][n][cu], like the global staging
     const int pb = s & 1;
-    if (!a.noxchg) {
+    if (!k_noxchg) {
       if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
       mbar_wait_cluster(&bars[2 + pb], (par_phase >> pb) & 1u);
       par_phase ^= 1u << pb;
     }
     FRNN_PROF(5, T - 1 - (s - 1));
-    if (own && pbf && (FX || a.pvec == 2)) {  // words [src][n][PW]: one word per source = units (u, u+1) of row b
+    if (own && pbf && a.pvec == 2) {  // words [src][n][PW]: one word per source = units (u, u+1) of row b
       const uint32_t* rp = reinterpret_cast<const uint32_t*>(pb ? recv1 : recv) + (size_t)b * PW + (u >> 1);
       const size_t qs = (size_t)N * PW;
       float t0 = 0.f, t1 = 0.f;
@@ -729,13 +753,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       }
       ds[0][0] += t0;
       ds[0][1] += t1;
-    } else if (own && pbf) {  // words [src][u/2][b/2][2] (push_pair_cols) or [src][b/2][cu]: units (u, u+1), half b&1
+    } else if ((!LEAN || a.pvec == 0) && own && pbf) {  // [src][u/2][b/2][2] (push_pair_cols) or [src][b/2][cu]: half b&1
       const uint32_t* rp = reinterpret_cast<const uint32_t*>(pb ? recv1 : recv) +
                            (a.pvec ? (size_t)(u >> 1) * N + (b >> 1) * 2 : (size_t)(b >> 1) * a.UPC + u);
       const size_t qs = (size_t)(N / 2) * a.UPC;
       float t0 = 0.f, t1 = 0.f;
       const int sh = (b & 1) ? 0 : 16;  // lo16 = bits << 16, hi16 = bits & 0xffff0000
-      if (FX || (a.CL == 16 && a.absu)) {  // all loads in flight first, then the fixed-order sums (deterministic)
+      if (FX || (a.CL == 16 && (LEAN || a.absu))) {  // all loads in flight first, then the fixed-order sums (deterministic)
         uint2 v[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) v[q] = *reinterpret_cast<const uint2*>(rp + q * qs);
@@ -761,7 +785,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       const float* rp = (pb ? recv1 : recv) + (size_t)b * a.UPC + u;
       const size_t qs = (size_t)N * a.UPC;
       float t0 = 0.f, t1 = 0.f;
-      if (FX || (a.CL == 16 && a.absu)) {  // all loads in flight first, then the fixed-order sums
+      if (FX || (a.CL == 16 && (LEAN || a.absu))) {  // all loads in flight first, then the fixed-order sums
         float2 v[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) v[q] = *reinterpret_cast<const float2*>(rp + q * qs);
@@ -786,7 +810,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     }
   };
   auto absorb = [&](int s) {
-    if (FX || a.dsm == 2) {
+    if (LEAN || a.dsm == 2) {
       absorb_rows(s);
       return;
     }
@@ -836,7 +860,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     float dgv[NG][2];
     // dx = dg for input-wired gates, engine.hpp:311-316 (off the critical path)
     auto store_dx = [&]() {
-      if (valid && !a.nodx) {
+      if (valid && !k_nodx) {
         bf16* dxg = dx + (size_t)t * gstep + xo;
 #pragma unroll
         for (int j = 0; j < NG; ++j) {
@@ -859,6 +883,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           for (int j = 0; j < NG; ++j) dg[j] = dsl[0];
 #pragma unroll
           for (int s = 0; s < NS; ++s) dsp[s] = dsl[s];
+        } else if (!csplit) {  // Jacobian formed and contracted here (cell.hpp:108-201, engine.hpp:275-284)
+          float prev[4], g[4];
+#pragma unroll
+          for (int s = 0; s < NS; ++s) prev[s] = h ? hi16(pv[s]) : lo16(pv[s]);
+#pragma unroll
+          for (int j = 0; j < NG; ++j) g[j] = h ? hi16(gv[j]) : lo16(gv[j]);
+          C::template bwd<M>(prev, g, dsl, dg, dsp);
         } else {
           C::apply(kc[h], dsl, dg, dsp);  // engine.hpp:275-284 with the coefficients formed last step
         }
@@ -881,6 +912,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         *reinterpret_cast<uint32_t*>(dgB + kmaj(b, u, N)) = (pk[0][0] & 0xFFFFu) | (pk[1][0] << 16);
     }
     load_dh(t - 1);
+    if (!csplit) load_trace(t - 1);  // (the fused Jacobian path: next step's trace, one step ahead)
     if (recur) {
       fence_proxy_async_smem();
       __syncthreads();
@@ -968,9 +1000,11 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     }
     // Under step t's MMAs: the Jacobian of step t-1 (its trace landed during step
     // t+1), then the trace loads for step t-2.
-    if (t > 0 && !a.skeleton) coefs();
-    load_trace(t - 2);
-    if (a.dxearly) store_dx();
+    if (csplit) {
+      if (t > 0 && !a.skeleton) coefs();
+      load_trace(t - 2);
+    }
+    if (dxearly) store_dx();
     if (recur) {
       FRNN_PROF(3, k);
       // partial R_p^T dg_p, column c -> owner CTA c / UPC, layout [dest][src][b][u];
@@ -997,7 +1031,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (e ? a1 : a0) * N, v);
           const uint32_t mbr = mapa_shared(rbar, q);
           if (FX || (pbf && a.pvec == 2)) {
-            push_col_pairs<N>(v, l, !a.noxchg, cu, pair_pitch(48), rb + (uint32_t)(me * N * pair_pitch(48) * 4), q, mbr);
+            push_col_pairs<N>(v, l, !k_noxchg, cu, pair_pitch(48), rb + (uint32_t)(me * N * pair_pitch(48) * 4), q, mbr);
           } else if (pbf && a.pvec) {
             push_pair_cols<N>(v, l, true, cu, rb + (uint32_t)(me * (N / 2) * 48 * 4), q, mbr);
           } else if (pbf) {  // words [src][n/2][cu] = bf16 (n even, n odd)
@@ -1039,16 +1073,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (sblk ? MBT + i : i) * N, v);
         if (FX || (pbf && a.pvec == 2)) {  // whole warp (shuffles inside)
           const int q = min(c / a.UPC, a.CL - 1), cu = c % a.UPC;  // (clamped for lanes past DH)
-          push_col_pairs<N>(v, l, lane_ok && c < DH && !a.noxchg, cu, PW, rb + (uint32_t)(me * N * PW * 4), q,
+          push_col_pairs<N>(v, l, lane_ok && c < DH && !k_noxchg, cu, PW, rb + (uint32_t)(me * N * PW * 4), q,
                             mapa_shared(rbar, q));
-        } else if (pbf && a.pvec) {  // whole warp (shuffles inside)
+        } else if (!LEAN && pbf && a.pvec) {  // whole warp (shuffles inside)
           const int q = min(c / a.UPC, a.CL - 1), cu = c % a.UPC;  // (clamped for lanes past DH)
           push_pair_cols<N>(v, l, lane_ok && c < DH, cu, rb + (uint32_t)(me * (N / 2) * a.UPC * 4), q,
                             mapa_shared(rbar, q));
         } else if (lane_ok && c < DH) {
           const bool u48 = a.UPC == 48;  // the H=768 tiling: constant divisor and stride
           const int q = u48 ? c / 48 : c / a.UPC, cu = u48 ? c % 48 : c % a.UPC;
-          if (a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
+          if (LEAN || a.dsm == 2) {  // 4-byte pushes into the owner's recv[t&1][me][n][cu]: a warp writes
                              // 32 consecutive columns = one contiguous 128-byte row segment per n
             const uint32_t mbr = mapa_shared(rbar, q);
             if (pbf) {
@@ -1066,12 +1100,12 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
 #pragma unroll
               for (int n = 0; n < N; ++n) st_async_b32(dst + (uint32_t)(n * a.UPC * 4), v[n], mbr);
             }
-          } else if (dsm) {  // push straight into the owner's recv[t&1][me][cu][:], completing bytes on its mbarrier
+          } else if (!LEAN && dsm) {  // push straight into the owner's recv[t&1][me][cu][:], on its mbarrier
             const uint32_t dst = mapa_shared(rb + (uint32_t)(((me * a.UPC + cu) * N) * 4), q);
             const uint32_t mbr = mapa_shared(rbar, q);
 #pragma unroll
             for (int i = 0; i < N / 4; ++i) st_async_v4(dst + 16 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3], mbr);
-          } else {
+          } else if (!LEAN) {
             float* dst = base + (((size_t)q * a.CL + me) * N) * a.UPC + cu;
 #pragma unroll
             for (int n = 0; n < N; ++n) dst[(size_t)n * a.UPC] = v[n];
@@ -1086,7 +1120,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       if (!dsm && tid < a.CL) mbar_arrive_remote(mapa_shared(smem_u32(&bars[2 + (t & 1)]), tid));
       FRNN_PROF(4, k);
     }
-    if (!a.dxearly) store_dx();
+    if (!dxearly) store_dx();
   }
   if (recur && T > 0) absorb(0);
   if (valid) {
@@ -1237,6 +1271,13 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.pvec = backward ? cs.pvec : 0;
 
   a.skeleton = g_skeleton || (getenv("FRNN_DBG_SKELETON") && atoi(getenv("FRNN_DBG_SKELETON")));
+  {
+    const char* cs_ = getenv("FRNN_COEFSPLIT");  // default: long MMA windows only
+    a.csplit = cs_ ? atoi(cs_) : ((cs.KBP / 16) * (cs.MBT + cs.MS) >= 48);
+  }
+  // backward single-gate cells keep the unit-fastest ownership (Elman 3.92 -> 3.30 us/step)
+  a.map = getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP") ? atoi(getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP"))
+                                                       : (backward && p.NG == 1 ? 0 : 1);
   a.hdirect = getenv("FRNN_HDIRECT") ? atoi(getenv("FRNN_HDIRECT")) : 1;  // fwd 2.52 -> 2.44 us/step
   a.xpf = getenv("FRNN_XPF") ? atoi(getenv("FRNN_XPF")) : 0;
   a.rot = getenv("FRNN_ROT") ? atoi(getenv("FRNN_ROT")) : 0;  // measured neutral-to-slower (DESIGN 8c)
@@ -1290,16 +1331,28 @@ bool bwd_fixed_layout(const CArgs& a, const ClusterShape& cs) {
 }
 
 using KernelFn = void (*)(CArgs);
+// The lean instance (L = 2) whenever the exchange is the default one.
+bool bwd_lean_layout(const CArgs& a) {
+  return a.dsm == 2 && (!a.pbf16 || a.pvec == 2 || a.pvec == 0) && a.absu && !getenv("FRNN_BWD_GENERIC");
+}
+
+// L = 3 (lean and plain) when no split coefficients and no experiment/debug switch is asked for.
+bool bwd_plain(const CArgs& a) { return !a.csplit && !a.rot && !a.dxearly && !a.noxchg && !a.nodx && !a.noload; }
+
 template <int V>
-KernelFn bwd_kernel(bool fixed) {
-  if constexpr (V == kElman) return cl_bwd_kernel<V, 16, 0>;
-  else return fixed ? cl_bwd_kernel<V, 16, 1> : cl_bwd_kernel<V, 16, 0>;
+KernelFn bwd_kernel(int L) {
+  if constexpr (V == kElman) {
+    return L == 3 ? cl_bwd_kernel<V, 16, 3> : L ? cl_bwd_kernel<V, 16, 2> : cl_bwd_kernel<V, 16, 0>;
+  } else {
+    return L == 1 ? cl_bwd_kernel<V, 16, 1> : L == 2 ? cl_bwd_kernel<V, 16, 2>
+         : L == 3 ? cl_bwd_kernel<V, 16, 3> : cl_bwd_kernel<V, 16, 0>;
+  }
 }
 
 template <bool BWD>
 cudaError_t launch_variant(int variant, const CArgs& a, const ClusterShape& cs, cudaStream_t s) {
   const int grid = cs.groups * cs.CL;
-  const bool fx = BWD && bwd_fixed_layout(a, cs);
+  const int fx = !BWD ? 0 : bwd_fixed_layout(a, cs) ? 1 : bwd_lean_layout(a) ? (bwd_plain(a) ? 3 : 2) : 0;
   using K = KernelFn;
   switch (variant) {
     case kElman:
