@@ -31,6 +31,10 @@ FRNN_API int frnn_debug_skeleton(int32_t enable);
  * FRNN_ALGO_ALTERNATING) for a shape, in the text form of flashrnn_csp.h. */
 FRNN_API int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
                                  int32_t algo, char* out, size_t out_bytes);
+/* The cluster tiling the planner launches for a pass: out10 = {algo, cluster,
+ * UPC, CL, MBT, MS, SSM, KBP, R1, R2} (zeros past `cluster` when not clustered). */
+FRNN_API int frnn_debug_cluster_shape(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                                      int32_t* out10);
 /* The placement half of frnn_dist_gather (flashrnn_dist.h) for a `world`-rank
  * layout, from a caller-filled staging buffer [world][blk] (what ncclAllGather
  * would deliver) into the full tensor k (0 states, 1 gates, 2 dx, 3 ds0, 4 dR,

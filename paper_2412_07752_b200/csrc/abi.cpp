@@ -571,6 +571,25 @@ int frnn_partition(frnn_shape shape, int32_t world_size, int32_t rank, frnn_shar
   return FRNN_OK;
 }
 
+int frnn_debug_cluster_shape(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass, int32_t* out10) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
+  if (!out10) return fail(FRNN_EINVAL_ARG, "null output");
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, pass, nullptr, &pl))) return rc;
+  for (int i = 0; i < 10; ++i) out10[i] = 0;
+  out10[0] = pl.algo;
+  out10[1] = pl.cluster;
+  if (pl.algo != FRNN_ALGO_FUSED || pl.cluster <= 0) return FRNN_OK;
+  const frnn::ClusterShape cs = frnn::cluster_shape(p, pl.units_per_cta, pl.batch_tile, pass == FRNN_PASS_BACKWARD);
+  const int32_t v[8] = {cs.UPC, cs.CL, cs.MBT, cs.MS, cs.SSM, cs.KBP, cs.R1, cs.R2};
+  for (int i = 0; i < 8; ++i) out10[2 + i] = v[i];
+  return FRNN_OK;
+}
+
 int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass, int32_t algo,
                         char* out, size_t out_bytes) {
   g_err.clear();

@@ -69,6 +69,7 @@ struct CArgs {
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
   int xpf;         // forward: L2 prefetch of x two steps ahead (FRNN_XPF)
+  int itab;        // backward: compile-time issue instances for the planner's tilings (FRNN_ISSUE_TABLE=0: loop)
   int csplit;      // backward: Jacobian coefficients under the previous MMA window (FRNN_COEFSPLIT)
   int map;         // element ownership (own_pair): 1 = row-fastest groups of 8, 0 = unit-fastest
   int hdirect;     // forward: cell threads write h straight to the global staging slice (FRNN_HDIRECT)
@@ -502,6 +503,27 @@ __device__ __noinline__ void issue_bwd_fixed(uint32_t tbase, uint32_t acc1, uint
     if (elect_one()) mma_commit(&blkbar[i]);
     __syncwarp();
   }
+}
+
+// Every backward tiling (TMEM blocks MBT, SMEM blocks MS of 128 columns, K steps
+// NK) the planner launches for 16 <= DH <= 1024 and any cell (enumerated with
+// scripts/tilings.py / frnn_debug_cluster_shape), each a straight-line issue
+// instance; (4,2,12), (6,0,3) and (2,0,12) are spelled out in the kernel.
+#define FRNN_BWD_TILINGS(X)                                                                                       \
+  X(1, 0, 1) X(1, 0, 2) X(1, 0, 3) X(1, 0, 4) X(1, 0, 8) X(1, 0, 10) X(1, 0, 12) X(2, 0, 1) X(2, 0, 2) X(2, 0, 3) \
+  X(2, 0, 4) X(2, 0, 8) X(2, 0, 10) X(3, 0, 2) X(3, 0, 3) X(3, 0, 8) X(3, 0, 10) X(3, 0, 12) X(4, 0, 2)          \
+  X(4, 0, 3) X(4, 0, 8) X(4, 0, 10) X(4, 0, 12) X(4, 1, 12) X(5, 0, 3) X(5, 0, 10) X(3, 4, 14)
+__device__ __forceinline__ bool issue_bwd_table(int MBT, int MS, int nk, uint32_t tbase, uint32_t acc1, uint64_t bd,
+                                                uint64_t ad, uint32_t idesc, uint32_t idesc2, uint64_t* blkbar) {
+  switch (MBT * 1000 + MS * 100 + nk) {
+#define FRNN_BWD_CASE(M_, S_, K_)                                   \
+  case M_ * 1000 + S_ * 100 + K_:                                   \
+    issue_bwd_fixed<M_, S_, K_>(tbase, acc1, bd, ad, idesc, idesc2, blkbar); \
+    return true;
+    FRNN_BWD_TILINGS(FRNN_BWD_CASE)
+#undef FRNN_BWD_CASE
+  }
+  return false;
 }
 
 // ----------------------------------------------------------- backward ----
@@ -961,14 +983,9 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           mma3_ts(acc + 5 * N, tbase + 5 * cb, bd, bk, idesc, 0);
           if (elect_one()) mma_commit(&blkbar[5]);
           __syncwarp();
-        } else if (N == 16 && MBT == 5 && MS == 0 && nk == 10 && !a.skeleton) {  // e.g. H=640, 4 gates
-          issue_bwd_fixed<5, 0, 10>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
-        } else if (N == 16 && MBT == 4 && MS == 0 && nk == 8 && !a.skeleton) {  // e.g. H=512, 4 gates
-          issue_bwd_fixed<4, 0, 8>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
-        } else if (N == 16 && MBT == 3 && MS == 0 && nk == 12 && !a.skeleton) {  // e.g. 2 heads of 384
-          issue_bwd_fixed<3, 0, 12>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
-        } else if (N == 16 && SSM == 128 && MBT == 3 && MS == 4 && nk == 14 && !a.skeleton) {
-          issue_bwd_fixed<3, 4, 14>(tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar);
+        } else if (!FX && N == 16 && SSM == 128 && !a.skeleton && a.itab &&
+                   issue_bwd_table(MBT, MS, nk, tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar)) {
+          // every other tiling the planner reaches: compile-time issue instance (scripts/tilings.py)
         } else if (MBT == 2 && MS == 0 && nk == 12 && !a.skeleton) {  // DH=192 per head (config 3)
           const uint64_t bk = (2 * LBO) >> 4;
           mma12_ts(tbase + a.acc1, tbase, bd, bk, idesc, 0);
@@ -1276,6 +1293,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
     a.csplit = cs_ ? atoi(cs_) : ((cs.KBP / 16) * (cs.MBT + cs.MS) >= 48);
   }
   // backward single-gate cells keep the unit-fastest ownership (Elman 3.92 -> 3.30 us/step)
+  a.itab = getenv("FRNN_ISSUE_TABLE") ? atoi(getenv("FRNN_ISSUE_TABLE")) : 1;
   a.map = getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP") ? atoi(getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP"))
                                                        : (backward && p.NG == 1 ? 0 : 1);
   a.hdirect = getenv("FRNN_HDIRECT") ? atoi(getenv("FRNN_HDIRECT")) : 1;  // fwd 2.52 -> 2.44 us/step
