@@ -83,6 +83,8 @@ struct Cell;
 template <>
 struct Cell<kElman> {
   static constexpr int NS = 1, NG = 1, NGP = 1;
+  static constexpr int NGK = 1;  // backward K rows per unit (gates with R); kgate: their gate index
+  static __host__ __device__ constexpr int kgate(int q) { return q; }
   static constexpr bool rec(int) { return true; }
   static constexpr bool inp(int) { return true; }
   template <class M>
@@ -111,6 +113,8 @@ struct Cell<kElman> {
 template <>
 struct Cell<kLstm> {
   static constexpr int NS = 2, NG = 4, NGP = 4;
+  static constexpr int NGK = 4;
+  static __host__ __device__ constexpr int kgate(int q) { return q; }
   static constexpr bool rec(int) { return true; }
   static constexpr bool inp(int) { return true; }
   template <class M>
@@ -172,6 +176,10 @@ struct Cell<kLstm> {
 template <>
 struct Cell<kGru> {
   static constexpr int NS = 1, NG = 4, NGP = 4;
+  // the n gate (j = 2) has no R (cell.hpp:43): the backward's R^T.dg contraction
+  // skips its rows -- K = 3 rows per unit instead of the padded 4
+  static constexpr int NGK = 3;
+  static __host__ __device__ constexpr int kgate(int q) { return q < 2 ? q : 3; }
   static constexpr bool rec(int j) { return j != 2; }  // n skips R   (cell.hpp:43)
   static constexpr bool inp(int j) { return j != 3; }  // g skips x   (cell.hpp:44)
   template <class M>
@@ -220,6 +228,8 @@ struct Cell<kGru> {
 template <>
 struct Cell<kSlstm> {
   static constexpr int NS = 4, NG = 4, NGP = 4;
+  static constexpr int NGK = 4;
+  static __host__ __device__ constexpr int kgate(int q) { return q; }
   static constexpr bool rec(int) { return true; }
   static constexpr bool inp(int) { return true; }
   template <class M>

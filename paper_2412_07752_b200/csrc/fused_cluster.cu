@@ -512,7 +512,8 @@ __device__ __noinline__ void issue_bwd_fixed(uint32_t tbase, uint32_t acc1, uint
 #define FRNN_BWD_TILINGS(X)                                                                                       \
   X(1, 0, 1) X(1, 0, 2) X(1, 0, 3) X(1, 0, 4) X(1, 0, 8) X(1, 0, 10) X(1, 0, 12) X(2, 0, 1) X(2, 0, 2) X(2, 0, 3) \
   X(2, 0, 4) X(2, 0, 8) X(2, 0, 10) X(3, 0, 2) X(3, 0, 3) X(3, 0, 8) X(3, 0, 10) X(3, 0, 12) X(4, 0, 2)          \
-  X(4, 0, 3) X(4, 0, 8) X(4, 0, 10) X(4, 0, 12) X(4, 1, 12) X(5, 0, 3) X(5, 0, 10) X(3, 4, 14)
+  X(4, 0, 3) X(4, 0, 8) X(4, 0, 10) X(4, 0, 12) X(4, 1, 12) X(5, 0, 3) X(5, 0, 10) X(3, 4, 14)            \
+  X(1, 0, 6) X(1, 0, 9) X(2, 0, 6) X(2, 0, 9) X(3, 0, 6) X(3, 0, 9) X(4, 0, 6) X(4, 0, 9) X(5, 0, 9) X(5, 1, 9)
 __device__ __forceinline__ bool issue_bwd_table(int MBT, int MS, int nk, uint32_t tbase, uint32_t acc1, uint64_t bd,
                                                 uint64_t ad, uint32_t idesc, uint32_t idesc2, uint64_t* blkbar) {
   switch (MBT * 1000 + MS * 100 + nk) {
@@ -530,7 +531,7 @@ __device__ __forceinline__ bool issue_bwd_table(int MBT, int MS, int nk, uint32_
 template <int V, int N, int L>  // L = 1: the H=768 4-gate layout (every tiling branch fixed at compile time)
 __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   using C = Cell<V>;
-  constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP;
+  constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP, NGK = C::NGK;
   using M = Math<true>;
   const Problem& p = a.p;
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, NT = blockDim.x;
@@ -609,7 +610,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     for (int ib = 0; ib < MS; ++ib) {
       uint8_t* blk = AS + ib * blk_bytes;
       for (int i = tid; i < SSM * KBP; i += NT) {
-        const int m = i % SSM, k = i / SSM, c = rotc(MBT * 128 + ib * SSM + m), uu = k / NGP, g = k % NGP;
+        const int m = i % SSM, k = i / SSM, c = rotc(MBT * 128 + ib * SSM + m), uu = k / NGK, g = C::kgate(k % NGK);
         const float v = (c < DH && uu < a.UPC && g < NG && p.rec[g])
                             ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
         *reinterpret_cast<bf16*>(blk + kmaj(m, k, SSM)) = __float2bfloat16_rn(v);
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           float f[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int row = 2 * (c0 + q) + h, uu = row / NGP, g = row % NGP;
+            const int row = 2 * (c0 + q) + h, uu = row / NGK, g = C::kgate(row % NGK);
             f[h] = (c < DH && uu < a.UPC && g < NG && p.rec[g])
                        ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
           }
@@ -925,8 +926,14 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) ds[s][h] = dsp[s];
       }
-      // The pair's NGP*2 gate rows are contiguous along K of the dg tile.
-      if (NGP == 4)
+      // The pair's NGK*2 gate rows are contiguous along K of the dg tile.
+      if (NGK == 3) {  // GRU: rows (u:z, u:r, u:g, u+1:z, u+1:r, u+1:g) from k = 3u, as 3 bf16 pairs
+        const uint32_t lo = pk[0][0], hi = pk[1][0];
+        const uint32_t g0 = pk[0][1] >> 16, g1 = pk[1][1] >> 16;  // dg of gate 3 (j = 3: high half)
+        *reinterpret_cast<uint32_t*>(dgB + kmaj(b, 3 * u, N)) = lo;
+        *reinterpret_cast<uint32_t*>(dgB + kmaj(b, 3 * u + 2, N)) = g0 | (hi << 16);
+        *reinterpret_cast<uint32_t*>(dgB + kmaj(b, 3 * u + 4, N)) = (hi >> 16) | (g1 << 16);
+      } else if (NGP == 4)
         *reinterpret_cast<uint4*>(dgB + kmaj(b, u * 4, N)) = make_uint4(pk[0][0], pk[0][1], pk[1][0], pk[1][1]);
       else if (NGP == 2)
         *reinterpret_cast<uint2*>(dgB + kmaj(b, u * 2, N)) = make_uint2(pk[0][0], pk[1][0]);
@@ -1189,7 +1196,9 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
   s.R1 = rows < 128 ? rows : 128;
   s.R2 = rows - s.R1;
   s.K = p.DH;
-  s.KBP = (rows + 15) / 16 * 16;
+  // backward K rows per unit: only gates with R (GRU's n gate has none, cell.hpp:43)
+  const int ngk = p.variant == kGru ? 3 : NGP;
+  s.KBP = (UPC * (backward ? ngk : NGP) + 15) / 16 * 16;
   s.MB = (p.DH + 127) / 128;
   s.slice = (uint32_t)UPC * N * 2;
   const int NBT = (p.B + N - 1) / N;
