@@ -69,6 +69,7 @@ struct CArgs {
   int dsm;         // backward partial exchange: 1 = DSMEM st.async pushes, 0 = global + TMA bulk load
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
   int xpf;         // forward: L2 prefetch of x two steps ahead (FRNN_XPF)
+  int kcompact;    // backward: GRU K rows without the n gate (gru_compact)
   int itab;        // backward: compile-time issue instances for the planner's tilings (FRNN_ISSUE_TABLE=0: loop)
   int csplit;      // backward: Jacobian coefficients under the previous MMA window (FRNN_COEFSPLIT)
   int map;         // element ownership (own_pair): 1 = row-fastest groups of 8, 0 = unit-fastest
@@ -531,7 +532,10 @@ __device__ __forceinline__ bool issue_bwd_table(int MBT, int MS, int nk, uint32_
 template <int V, int N, int L>  // L = 1: the H=768 4-gate layout (every tiling branch fixed at compile time)
 __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   using C = Cell<V>;
-  constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP, NGK = C::NGK;
+  constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP;
+  // backward K rows per unit: the padded NGP, or (a.kcompact, GRU) only the gates with R
+  const int NGK = a.kcompact ? C::NGK : NGP;
+  auto kgate = [&](int q) { return a.kcompact ? C::kgate(q) : q; };
   using M = Math<true>;
   const Problem& p = a.p;
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, NT = blockDim.x;
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     for (int ib = 0; ib < MS; ++ib) {
       uint8_t* blk = AS + ib * blk_bytes;
       for (int i = tid; i < SSM * KBP; i += NT) {
-        const int m = i % SSM, k = i / SSM, c = rotc(MBT * 128 + ib * SSM + m), uu = k / NGK, g = C::kgate(k % NGK);
+        const int m = i % SSM, k = i / SSM, c = rotc(MBT * 128 + ib * SSM + m), uu = k / NGK, g = kgate(k % NGK);
         const float v = (c < DH && uu < a.UPC && g < NG && p.rec[g])
                             ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
         *reinterpret_cast<bf16*>(blk + kmaj(m, k, SSM)) = __float2bfloat16_rn(v);
@@ -631,7 +635,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           float f[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int row = 2 * (c0 + q) + h, uu = row / NGK, g = C::kgate(row % NGK);
+            const int row = 2 * (c0 + q) + h, uu = row / NGK, g = kgate(row % NGK);
             f[h] = (c < DH && uu < a.UPC && g < NG && p.rec[g])
                        ? bf(R, ((size_t)(hd * NG + g) * DH + unit0 + uu) * DH + c) : 0.f;
           }
@@ -927,7 +931,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         for (int s = 0; s < NS; ++s) ds[s][h] = dsp[s];
       }
       // The pair's NGK*2 gate rows are contiguous along K of the dg tile.
-      if (NGK == 3) {  // GRU: rows (u:z, u:r, u:g, u+1:z, u+1:r, u+1:g) from k = 3u, as 3 bf16 pairs
+      if (C::NGK == 3 && a.kcompact) {  // GRU: rows (u:z, u:r, u:g, u+1:z, u+1:r, u+1:g) from k = 3u, as 3 bf16 pairs
         const uint32_t lo = pk[0][0], hi = pk[1][0];
         const uint32_t g0 = pk[0][1] >> 16, g1 = pk[1][1] >> 16;  // dg of gate 3 (j = 3: high half)
         *reinterpret_cast<uint32_t*>(dgB + kmaj(b, 3 * u, N)) = lo;
@@ -1183,6 +1187,13 @@ uint32_t pow2_cols(uint32_t c) {
 
 int ngp_of(int NG) { return NG <= 1 ? 1 : NG <= 2 ? 2 : 4; }
 int NSof(const Problem& p) { return p.NS; }
+// GRU backward without the n gate's zero R rows in K (FRNN_GRU_COMPACT=1): correct
+// and 25 % fewer MMAs, but measured slower at H=768 (the padded layout keeps the
+// compile-time headline instance) -- off by default
+bool gru_compact(const Problem& p) {
+  const char* e = getenv("FRNN_GRU_COMPACT");
+  return p.variant == kGru && e && atoi(e) != 0;
+}
 
 }  // namespace
 
@@ -1197,7 +1208,7 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
   s.R2 = rows - s.R1;
   s.K = p.DH;
   // backward K rows per unit: only gates with R (GRU's n gate has none, cell.hpp:43)
-  const int ngk = p.variant == kGru ? 3 : NGP;
+  const int ngk = gru_compact(p) ? 3 : NGP;
   s.KBP = (UPC * (backward ? ngk : NGP) + 15) / 16 * 16;
   s.MB = (p.DH + 127) / 128;
   s.slice = (uint32_t)UPC * N * 2;
@@ -1302,6 +1313,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
     a.csplit = cs_ ? atoi(cs_) : ((cs.KBP / 16) * (cs.MBT + cs.MS) >= 48);
   }
   // backward single-gate cells keep the unit-fastest ownership (Elman 3.92 -> 3.30 us/step)
+  a.kcompact = backward && gru_compact(p);
   a.itab = getenv("FRNN_ISSUE_TABLE") ? atoi(getenv("FRNN_ISSUE_TABLE")) : 1;
   a.map = getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP") ? atoi(getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP"))
                                                        : (backward && p.NG == 1 ? 0 : 1);

@@ -200,6 +200,15 @@ def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
     check_bf16(eng, orc, v, inp)
 
 
+@pytest.mark.parametrize("NH,DH", [(1, 768), (1, 512), (2, 96)])
+def test_bf16_gru_compact_k(eng, orc, monkeypatch, NH, DH):
+    """GRU backward with the n gate's (zero) R rows dropped from the R^T.dg K
+    dimension (FRNN_GRU_COMPACT=1, cell.hpp:43): same results as the padded layout."""
+    monkeypatch.setenv("FRNN_GRU_COMPACT", "1")
+    inp = orc.generate("gru", 12, 16, NH, DH, seed=5)
+    check_bf16(eng, orc, "gru", inp)
+
+
 @pytest.mark.parametrize("B", [5, 24, 40, 48, 96, 130])
 def test_bf16_dr_gemm_any_batch(eng, orc, B):
     """dR / db through the tcgen05 dR GEMM (dr_gemm.cu) at batch sizes that do
