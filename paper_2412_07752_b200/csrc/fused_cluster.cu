@@ -70,6 +70,7 @@ struct CArgs {
   int pbf16;       // dsm 2: push the partials as bf16 pairs (half the exchange bytes and pushes)
   int xpf;         // forward: L2 prefetch of x two steps ahead (FRNN_XPF)
   int kcompact;    // backward: GRU K rows without the n gate (gru_compact)
+  int waitmode;    // MMA-completion waits of non-issuing warps: 0 test_wait spin, 1 try_wait (FRNN_WAITMODE)
   int itab;        // backward: compile-time issue instances for the planner's tilings (FRNN_ISSUE_TABLE=0: loop)
   int csplit;      // backward: Jacobian coefficients under the previous MMA window (FRNN_COEFSPLIT)
   int map;         // element ownership (own_pair): 1 = row-fastest groups of 8, 0 = unit-fastest
@@ -374,7 +375,8 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
           if (p.inp[j]) prefetch_l2(xq + (size_t)j * D);
       }
     }
-    mbar_wait(&bars[0], t & 1);
+    if (w == 0) mbar_wait(&bars[0], t & 1);  // (the issuing warp spins)
+    else mbar_wait_idle(&bars[0], t & 1, a.waitmode);
     tc_fence_after();
     FRNN_PROF(2, t);
     // accumulators -> xs[b][row]: warps 0-3 drain the M=128 block, warps 4-7 (same
@@ -1051,7 +1053,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
                   a1 = wg == 0 ? 5 : wg == 1 ? 2 : 3;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          mbar_wait(&blkbar[e ? i1 : i0], mma_phase);
+          mbar_wait_idle(&blkbar[e ? i1 : i0], mma_phase, a.waitmode);
           FRNN_PROF_AT(6, k, NT - 32);  // the last warp's last block complete
           tc_fence_after();
           const int c = rotc((e ? c1 : c0) + 32 * qd + l), q = c / 48, cu = c % 48;
@@ -1083,7 +1085,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           i = both + (ent - 2 * both);
           sblk = MS > MBT;
         }
-        mbar_wait(&blkbar[i], mma_phase);
+        mbar_wait_idle(&blkbar[i], mma_phase, a.waitmode);
         FRNN_PROF_AT(6, k, NT - 32);  // the last warp's last block complete
         tc_fence_after();
         int c;
@@ -1314,6 +1316,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   }
   // backward single-gate cells keep the unit-fastest ownership (Elman 3.92 -> 3.30 us/step)
   a.kcompact = backward && gru_compact(p);
+  a.waitmode = getenv("FRNN_WAITMODE") ? atoi(getenv("FRNN_WAITMODE")) : 0;
   a.itab = getenv("FRNN_ISSUE_TABLE") ? atoi(getenv("FRNN_ISSUE_TABLE")) : 1;
   a.map = getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP") ? atoi(getenv(backward ? "FRNN_BMAP" : "FRNN_FMAP"))
                                                        : (backward && p.NG == 1 ? 0 : 1);

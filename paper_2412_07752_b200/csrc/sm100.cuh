@@ -567,6 +567,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!(g_spin_wait ? mbar_test(a, phase) : mbar_try_sleep(a, phase, 1000000u)))
     if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
 }
+// Waits for threads that are NOT on the issue path (the MMA-completion waits of
+// the drain / cell warps): mode 1 = mbarrier.try_wait without a time hint (the
+// hardware suspends the thread until the phase completes or a system-dependent
+// timeout, instead of hammering shared memory with test_wait probes while the
+// tensor core streams its operands from SMEM); mode 0 = the test_wait spin.
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t phase, int mode) {
+  if (mode == 0) {
+    mbar_wait(bar, phase);
+    return;
+  }
+  const uint32_t a = smem_u32(bar);
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t n = 0;
+  while (!mbar_try(a, phase))
+    if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > 4000000000ull) __trap();
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
