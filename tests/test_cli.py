@@ -24,6 +24,12 @@ def cli():
     return lambda *args: subprocess.run([EXE, *map(str, args)], capture_output=True, text=True)
 
 
+def test_plan_rejects_bad_dtype_and_pass(cli):
+    """Usage errors exit 2 like the reference CLI (main.cpp:4-5): no silent fallback to bf16."""
+    assert cli("plan", "--variant", "lstm", "--dtype", "fp16").returncode == 2
+    assert cli("plan", "--variant", "lstm", "--pass", "sideways").returncode == 2
+
+
 def test_plan_json(cli):
     r = cli("plan", "--variant", "slstm", "--head-dim", 3072, "--batch", 64)
     assert r.returncode == 0, r.stderr

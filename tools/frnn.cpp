@@ -108,8 +108,11 @@ int cmd_plan(const Args& a) {
   const frnn_cell c = cell_c(variant_of(a));
   const frnn_shape sh{(int32_t)a.num("seq", 1024), (int32_t)a.num("batch", 16), (int32_t)a.num("heads", 1),
                       (int32_t)a.num("head-dim", 768)};
-  const int dtype = a.str("dtype", "bf16") == "fp32" ? FRNN_F32 : FRNN_BF16;
-  const std::string pass = a.str("pass", "both");
+  const std::string ds = a.str("dtype", "bf16"), pass = a.str("pass", "both");
+  if (ds != "bf16" && ds != "fp32") throw std::invalid_argument("--dtype must be bf16 or fp32");  // exit 2
+  if (pass != "both" && pass != "forward" && pass != "backward")
+    throw std::invalid_argument("--pass must be forward, backward or both");
+  const int dtype = ds == "fp32" ? FRNN_F32 : FRNN_BF16;
   std::string out = "{";
   bool ok = true;
   for (int p : {0, 1}) {
