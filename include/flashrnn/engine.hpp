@@ -345,10 +345,13 @@ struct Staging {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
+  // The stream is deliberately never destroyed: a ForwardTrace may outlive the
+  // thread that produced it, and its device copy is freed stream-ordered on
+  // this stream (DevMem).  One stream per calling thread for the process lifetime.
   ~Staging() {
+    if (stream) cudaStreamSynchronize(stream);
     for (auto e : events) cudaEventDestroy(e);
     if (pin) cudaFreeHost(pin);
-    if (stream) cudaStreamDestroy(stream);
   }
   uint8_t* pinned(std::size_t bytes) {
     if (bytes > pin_bytes) {
