@@ -18,15 +18,24 @@
 // profiles/r01_allgather_microbench.txt.)
 //
 // Per backward step each CTA computes the partial R_p^T dg_p for all DH state
-// columns (A = R_p^T resident: MBT 128-column blocks in TMEM, the rest in SMEM),
-// stores it fp32 to global staging laid out [dest][src][b][u], and releases one
-// remote mbarrier arrive to every CTA; each CTA then pulls its [all src] block
-// with one TMA bulk load and sums the CL partials (+ clip, engine.hpp:300-303).
+// columns (A = R_p^T resident: MBT 128-column blocks in TMEM, MS in SMEM), one
+// tcgen05.commit per block pair; as each block completes, its drain lanes push
+// the partials straight into the owner CTA's shared memory (st.async with
+// mbarrier complete_tx, DSMEM), as bf16 column pairs for 4-gate cells (fp32
+// otherwise); the owner sums the CL sources in a fixed order (deterministic),
+// clips (engine.hpp:300-303) and applies the Jacobian -- whose coefficients
+// were formed under the previous step's MMAs for long MMA windows
+// (cells.cuh coef/apply).  FRNN_XCHG=0 keeps the round-1 global-staging
+// exchange (stores + TMA bulk load) for A/B.
 //
 // Element work: NT = up to 384 threads (3 warps per scheduler, so ALU/MUFU
 // latencies overlap); each thread owns a PAIR of adjacent units of one batch
-// row, so trace/x/dx traffic is bf16x2 and the dg tile gets 16-byte stores.
-// MMAs are issued by warp 0 as whole-warp PTX loops (sm100.cuh mma_chain_*).
+// row (own_pair: eight consecutive threads take eight consecutive rows, so
+// the dg-tile / h-slice stores are bank-conflict free), trace/x/dx traffic is
+// bf16x2.  MMAs are issued by warp 0 as straight-line PTX blocks (sm100.cuh
+// mma8_* / mma12_*, issue_bwd_fixed for every tiling the planner reaches).
+// Backward instances: L = 0 generic (all A/B switches), 1 the H=768 4-gate
+// layout, 2 / 3 lean (default exchange only; 3 also without split coefficients).
 #include <cuda_bf16.h>
 
 #include <algorithm>
