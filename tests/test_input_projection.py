@@ -31,8 +31,11 @@ def test_abi_validation_without_gpu():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("T,B,Din,NG,D", [(5, 3, 96, 4, 80), (7, 16, 64, 1, 256), (3, 21, 200, 4, 48)])
+@pytest.mark.parametrize("T,B,Din,NG,D", [(5, 3, 96, 4, 80), (7, 16, 64, 1, 256), (3, 21, 200, 4, 48),
+                                          (4, 5, 64, 1, 36), (9, 40, 136, 3, 200), (300, 9, 64, 4, 72)])
 def test_ragged_shapes(T, B, Din, NG, D):
+    """Token and gate tails inside a 256x256 pair tile, a K tail (Din=200, 136),
+    out_features % 8 != 0 (the single-CTA kernel) and more tiles than pairs."""
     import torch
     from paper_2412_07752_b200 import FlashRNN
     g = torch.Generator(device="cuda").manual_seed(T * 100 + Din)
@@ -72,3 +75,25 @@ def test_headline_shape_and_throughput():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     print(f"input projection {T * B}x{N}x{Din}: {ms * 1e3:.1f} us, {2 * T * B * N * Din / ms / 1e9:.0f} TFLOP/s")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["1", "2"])
+def test_full_output_vs_torch_fp32(algo, monkeypatch):
+    """Every element of the headline-sized projection against a torch fp32
+    matmul of the same bf16 inputs, for both kernels (FRNN_WX_ALGO=1: 128x256
+    single-CTA tiles; default: CTA-pair 256x256 persistent)."""
+    import torch
+    from paper_2412_07752_b200 import FlashRNN
+    monkeypatch.setenv("FRNN_WX_ALGO", algo)
+    T, B, Din, N = 1024, 16, 768, 3072
+    g = torch.Generator(device="cuda").manual_seed(11)
+    u = torch.randn(T, B, Din, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, Din, device="cuda", generator=g) / Din ** 0.5).bfloat16()
+    x = FlashRNN().input_projection(W, u)
+    ref = u.float().reshape(-1, Din) @ W.float().T
+    got = x.float().reshape(-1, N)
+    err = ((got - ref).norm() / ref.norm()).item()
+    worst = ((got - ref).abs() / (ref.abs() + 1e-2)).max().item()
+    assert err <= TOL, err
+    assert worst <= 2 ** -7, worst   # each element within one bf16 rounding of the fp32 sum
