@@ -140,14 +140,18 @@ __global__ void __launch_bounds__(128, 2)
 // columns), so the epilogue of tile i (warps 4-7: TMEM -> bf16 -> 128B-swizzled
 // smem -> TMA store) overlaps the mainloop of tile i+1.  Grid = one pair per
 // TPC, tiles strided over pairs.
-constexpr int P_BM = 128, P_BN = 256, P_ST = 5;
+constexpr int P_BM = 128, P_BN = 256, P_MAXST = 6;
 constexpr uint32_t P_A = P_BM * BK * 2, P_B = (P_BN / 2) * BK * 2, P_STAGE = P_A + P_B;  // 16 KB + 16 KB
 constexpr uint32_t P_OUT = P_BM * 64 * 2;                                                 // 128 rows x 128 B
-constexpr size_t P_SMEM = 1024 + P_ST * P_STAGE + 2 * P_OUT + 256;
+inline size_t pair_smem(int stages) { return 1024 + 2 * P_OUT + stages * P_STAGE + 256; }
 
 struct PArgs {
-  int tiles_n, tiles, numk;
+  int tiles_n, tiles_m, tiles, numk, stages, mfast;
 };
+// Tile t -> (token block, gate block): gate blocks fastest by default, so the
+// pairs in flight share token slabs of u.
+__device__ __forceinline__ int tile_m(const PArgs& g, int t) { return g.mfast ? t % g.tiles_m : t / g.tiles_n; }
+__device__ __forceinline__ int tile_n(const PArgs& g, int t) { return g.mfast ? t / g.tiles_m : t % g.tiles_n; }
 
 __device__ __forceinline__ void tma_load_2d_pair(void* smem, const void* map, int c0, int c1, uint32_t leader_bar) {
   asm volatile(
@@ -192,8 +196,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                         const __grid_constant__ CUtensorMap mapX, PArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* outbuf = smem + P_ST * P_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 2 * P_OUT);
+  uint8_t* outbuf = smem;
+  smem += 2 * P_OUT;
+  const uint32_t P_ST = g.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_ST * P_STAGE);
   uint64_t* empty = full + P_ST;
   uint64_t* tfull = empty + P_ST;
   uint64_t* tempty = tfull + 2;
@@ -207,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   if (tid == 32) {
-    for (int s = 0; s < P_ST; ++s) {
+    for (uint32_t s = 0; s < P_ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -232,8 +238,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const uint32_t leader_full = mapa_shared(smem_u32(full), 0);
       uint32_t it = 0;
       for (int t = pair; t < g.tiles; t += npairs) {
-        const int m0 = (t / g.tiles_n) * 2 * P_BM + (int)rank * P_BM;
-        const int n0 = (t % g.tiles_n) * P_BN + (int)rank * (P_BN / 2);
+        const int m0 = tile_m(g, t) * 2 * P_BM + (int)rank * P_BM;
+        const int n0 = tile_n(g, t) * P_BN + (int)rank * (P_BN / 2);
         for (int kb = 0; kb < g.numk; ++kb, ++it) {
           const uint32_t s = it % P_ST;
           if (it >= P_ST) mbar_wait(&empty[s], ((it / P_ST) - 1) & 1);
@@ -275,8 +281,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     uint32_t tl = 0, chunk = 0;
     for (int t = pair; t < g.tiles; t += npairs, ++tl) {
       const uint32_t acc = tl & 1;
-      const int m0 = (t / g.tiles_n) * 2 * P_BM + (int)rank * P_BM;
-      const int n0 = (t % g.tiles_n) * P_BN;
+      const int m0 = tile_m(g, t) * 2 * P_BM + (int)rank * P_BM;
+      const int n0 = tile_n(g, t) * P_BN;
       mbar_wait_cluster(&tfull[acc], (tl >> 1) & 1);
       tc_fence_after();
       for (int c = 0; c < P_BN; c += 64, ++chunk) {
@@ -364,16 +370,16 @@ cudaError_t wx_gemm(const void* W, const void* u, void* x, long long M, int N, i
     const long long tiles_m = (M + 2 * P_BM - 1) / (2 * P_BM);
     if (tiles_m * pa.tiles_n > (1ll << 30)) return cudaErrorInvalidValue;
     pa.tiles = (int)(tiles_m * pa.tiles_n);
+    pa.tiles_m = (int)tiles_m;
+    pa.mfast = getenv("FRNN_WX_RASTER") ? atoi(getenv("FRNN_WX_RASTER")) : 0;
     pa.numk = (K + BK - 1) / BK;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(wx_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)P_SMEM);
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
+    const char* st_env = getenv("FRNN_WX_PST");
+    pa.stages = st_env ? std::max(2, std::min(P_MAXST, atoi(st_env))) : 5;
+    cudaError_t e = cudaFuncSetAttribute(wx_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pair_smem(P_MAXST));
+    if (e != cudaSuccess) return e;
     const int pairs = std::min(sm_count() / 2, pa.tiles);
-    wx_gemm_pair_kernel<<<2 * pairs, 256, P_SMEM, s>>>(mu2, mw2, mx, pa);
+    wx_gemm_pair_kernel<<<2 * pairs, 256, pair_smem(pa.stages), s>>>(mu2, mw2, mx, pa);
     note_launch();
     return cudaGetLastError();
   }
