@@ -91,6 +91,12 @@ struct CArgs {
   int absu;        // absorb: CL == 16 unrolled (all loads first) -- A/B knob FRNN_ABSU
   int pvec;        // pbf16: [cu/2][n/2][2] layout, two 16-byte pushes per lane (push_pair_cols);
                    //        0 = [n/2][cu] layout, N/2 4-byte pushes per lane
+  int NCL;         // forward: clusters per group; > 1: slices of other clusters imported through L2
+  int Ks;          // forward: K columns of the R rows in SMEM (M=128 SS, second accumulator)
+  uint32_t* xflags;  // forward, NCL > 1: [groups][NCL*CL] step counters of the published slices
+  int mcfence, mcpoll;  // NCL > 1: full fence before the flag release; relaxed polling (A/B knobs)
+  int mcwarp, mclocal;  // NCL > 1: the importing warp; own cluster's K range issued first (A/B knobs)
+  int mcrelw;           // NCL > 1: the importing warp (not thread 0) releases the slice flag
   int skeleton;    // 1: synchronisation skeleton only -- no MMAs, no cell math (the sequential-
                    //    dependency floor of SURVEY 8d; frnn_debug_skeleton, results are garbage)
 };
@@ -201,7 +207,25 @@ __device__ __noinline__ void issue_fwd_fixed(uint32_t d1, uint32_t ta, uint32_t 
 }
 
 // ------------------------------------------------------------ forward ----
-template <int V, int N>
+// Steps [k0, k1) (16-wide K steps) of a K-split block: steps below nts have A in
+// TMEM (accumulator d1), the rest A in the SMEM M=128 tile (d2), issued
+// interleaved by one uniform PTX loop.  ts / ss: that accumulator already holds
+// a partial sum (updated).
+__device__ __forceinline__ void ksplit_range(uint32_t d1, uint32_t ta, int nts, uint32_t d2, uint64_t a2, uint64_t a2k,
+                                             uint64_t bd, uint64_t bk, uint32_t id, int k0, int k1, int& ts,
+                                             int& ss) {
+  const int ks0 = max(k0, nts);
+  const int n1 = max(0, min(k1, nts) - k0), n2 = max(0, k1 - ks0);
+  mma_chain_ksplit(d1, ta + 8u * k0, bd + (uint64_t)k0 * bk, n1, ts, d2, a2 + (uint64_t)(ks0 - nts) * a2k, a2k,
+                   bd + (uint64_t)ks0 * bk, n2, ss, bk, id);
+  ts |= n1 > 0;
+  ss |= n2 > 0;
+}
+
+// MC = 1: the multi-cluster / K-split instance (NCL > 1 or Ks > 0); MC = 0 keeps
+// the single-cluster code free of those branches (its register allocation and
+// scheduling are what the headline numbers were measured with).
+template <int V, int N, int MC>
 __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   using C = Cell<V>;
   constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP;
@@ -209,11 +233,15 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   const Problem& p = a.p;
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, NT = blockDim.x;
   const uint32_t me = cluster_ctarank();
-  const int grp = blockIdx.x / a.CL;
+  const int NCL = MC ? a.NCL : 1, Ks = MC ? a.Ks : 0;
+  const int NSL = a.CL * NCL;                             // h slices per group
+  const int grp = blockIdx.x / NSL;
+  const int cl = MC ? (blockIdx.x / a.CL) % NCL : 0;      // this CTA's cluster within the group
+  const int gq = MC ? cl * a.CL + (int)me : (int)me;      // this CTA's slice (unit block) within the group
   const int hd = grp / a.NBT, b0 = (grp % a.NBT) * N;
   const int nb = min(N, p.B - b0);
-  const int unit0 = me * a.UPC;
-  const int DH = p.DH, D = p.D, B = p.B, K = a.K, T = p.T;
+  const int unit0 = gq * a.UPC;
+  const int DH = p.DH, D = p.D, B = p.B, K = a.K, T = p.T, Kt = a.K - Ks;
   // xs[b][row'] with row' = row + 4*(row/32): a pad of 4 words per 32 rows makes
   // both the TMEM drain (consecutive rows) and the pointwise float4 reads (8
   // consecutive rows per thread) bank-conflict free.
@@ -228,15 +256,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* hB0 = smem;                       // [N x K] K-major (step parity 0)
   uint8_t* hB1 = hB0 + N * K * 2;            // (step parity 1)
-  uint8_t* A2 = hB1 + N * K * 2;             // [64 x K] K-major, rows R1..R1+R2
-  float* xs = reinterpret_cast<float*>(A2 + (a.R2 ? 64 * K * 2 : 0));  // [N][ROWS+1]
+  uint8_t* A2 = hB1 + N * K * 2;             // [64 x K] K-major, rows R1..R1+R2 (or [128 x Ks]: K split)
+  float* xs = reinterpret_cast<float*>(A2 + (a.R2 ? 64 * K * 2 : 128 * Ks * 2));  // [N][ROWS+1]
   uint8_t* hs = reinterpret_cast<uint8_t*>(xs + N * XP);               // my h slice
   uint64_t* bars = reinterpret_cast<uint64_t*>(hs + ((a.slice + 15) & ~15u));  // mma, x0, x1
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bars + 3);
+  // bars: MMA done, h(t) parity 0/1 (own cluster's slices), MC: other clusters' slices parity 0/1
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(bars + (MC ? 5 : 3));
 
   if (w == 0) tmem_alloc(tbase_s, a.tmem_cols);
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < (MC ? 5 : 3); ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < 2 * N * K * 2 / 16; i += NT) reinterpret_cast<uint4*>(hB0)[i] = make_uint4(0, 0, 0, 0);
@@ -249,6 +278,15 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, 64)) = v;
     }
   }
+  if (Ks) {  // K columns Kt.. of rows 0..R1-1 -> SMEM, K-major M=128 tile
+    for (int i = tid; i < 128 * (Ks / 8); i += NT) {
+      const int m = i % 128, kc = i / 128, u = m / NGP, g = m % NGP;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (m < a.R1 && g < NG && p.rec[g])
+        v = *reinterpret_cast<const uint4*>(R + ((size_t)(hd * NG + g) * DH + unit0 + u) * DH + Kt + kc * 8);
+      *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, 128)) = v;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -257,13 +295,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
     const int row = 32 * w + l, u = row / NGP, g = row % NGP;
     const bool valid = row < a.R1 && g < NG && p.rec[g];
     const bf16* src = R + ((size_t)(hd * NG + (valid ? g : 0)) * DH + unit0 + (valid ? u : 0)) * DH;
-    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+    for (int c0 = 0; c0 < Kt / 2; c0 += 16) {
       uint32_t v[16];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int k = 2 * c0 + 8 * q;
         uint4 r4 = make_uint4(0, 0, 0, 0);
-        if (valid && k < DH) r4 = *reinterpret_cast<const uint4*>(src + k);
+        if (valid && k < DH && k < Kt) r4 = *reinterpret_cast<const uint4*>(src + k);
         v[4 * q] = r4.x;
         v[4 * q + 1] = r4.y;
         v[4 * q + 2] = r4.z;
@@ -314,7 +352,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         *reinterpret_cast<const uint4*>(s0 + (size_t)(b0 + bb) * D + hd * DH + kc * 8);
   }
   fence_proxy_async_smem();
-  if (tid == 0) mbar_arrive_expect_tx(&bars[2], (uint32_t)a.CL * a.slice);  // step 1's h
+  if (tid == 0) {  // step 1's h
+    mbar_arrive_expect_tx(&bars[2], (uint32_t)a.CL * a.slice);
+    if (NCL > 1) mbar_arrive_expect_tx(&bars[4], (uint32_t)(NCL - 1) * a.CL * a.slice);
+  }
   __syncthreads();
   cluster_sync_all();  // all barriers initialised + armed before any multicast
 
@@ -330,6 +371,28 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       tc_fence_after();
       const uint64_t bd = sdesc_kmajor(smem_u32(buf ? hB1 : hB0), LBO, SBO);
       if (a.skeleton) {
+      } else if (MC) {
+        // One M=128 block, K split TMEM | SMEM.  The own cluster's K range first
+        // (its slices arrive by multicast ~1 k cycles after publishing), then the
+        // other clusters' slices once their L2 imports have landed.
+        const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 128 * 16, 128), a2k = (2 * 128 * 16) >> 4, bk = (2 * LBO) >> 4;
+        const int nk = K / 16, span = a.CL * a.UPC / 16, k0 = cl * span;
+        int ts = 0, ss = 0;
+        if (NCL > 1 && !a.mclocal) {  // A/B: everything after both barriers, natural K order
+          if (t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
+          tc_fence_after();
+          ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, 0, nk, ts, ss);
+        } else {
+        ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, k0, k0 + span, ts, ss);
+        if (NCL > 1) {
+          if (t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
+          FRNN_PROF(5, t);
+          tc_fence_after();
+          ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, 0, k0, ts, ss);
+          ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, k0 + span, nk, ts,
+                       ss);
+        }
+        }
       } else if (a.R2 && K == 768) {  // H=768 per head: 6 blocks of 8 K-steps, spelled out
         const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 64 * 16, 128);
         constexpr uint64_t a2k = (2 * 64 * 16) >> 4, bk = (2 * LBO) >> 4;
@@ -393,6 +456,12 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
     if (w < 4) {
       float v[16];
       tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc1, v);
+      if (Ks) {
+        float v2[16];
+        tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc2, v2);
+#pragma unroll
+        for (int n = 0; n < N; ++n) v[n] += v2[n];
+      }
       if (32 * w + l < a.R1) {
 #pragma unroll
         for (int n = 0; n < N; ++n) xs[n * XP + xs_row(32 * w + l)] = v[n];
@@ -408,7 +477,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
     }
     tc_fence_before();
     __syncthreads();
-    FRNN_PROF(5, t);
+    if (!MC) FRNN_PROF(5, t);
     float gout[NG][2], nout[NS][2];
     if (own) {
       float y[2][4];  // the pair's 2*NGP consecutive gate rows at column b
@@ -442,10 +511,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) st[s][h] = nout[s][h] = nx[s];
       }
-      FRNN_PROF(6, t);
+      if (!MC) FRNN_PROF(6, t);
       const uint32_t hword = b < nb ? pack_bf16(nout[0][0], nout[0][1]) : 0u;  // padding rows stay zero
       if (a.hdirect && t + 1 < T) {  // straight into the global staging slice (the multicast source)
-        uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + ((t + 1) & 1)) * a.CL + me) * a.slice;
+        uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + ((t + 1) & 1)) * NSL + gq) * a.slice;
         *reinterpret_cast<uint32_t*>(gst + kmaj(b, u, N)) = hword;
         fence_proxy_async_global();  // this writer's generic store -> the multicast's async-proxy read
       } else {
@@ -456,7 +525,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
     FRNN_PROF(3, t);
     if (t + 1 < T) {  // publish h_{t+1}: slice -> global staging -> multicast to the cluster
       const int nbuf = (t + 1) & 1;
-      uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + nbuf) * a.CL + me) * a.slice;
+      uint8_t* gst = reinterpret_cast<uint8_t*>(a.xstage) + (((size_t)grp * 2 + nbuf) * NSL + gq) * a.slice;
       if (!a.hdirect) {
         for (int i = tid; i < (int)(a.slice / 16); i += NT)
           reinterpret_cast<uint4*>(gst)[i] = reinterpret_cast<const uint4*>(hs)[i];
@@ -464,10 +533,50 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         __syncthreads();
       }
       FRNN_PROF(7, t);
+      if constexpr (!MC) {
+        if (tid == 0) {
+          mbar_arrive_expect_tx(&bars[1 + buf], (uint32_t)a.CL * a.slice);  // re-arm for step t+2
+          fence_proxy_async_global();
+          bulk_g2s_multicast((nbuf ? hB1 : hB0) + me * a.slice, gst, a.slice, &bars[1 + nbuf], mask);
+        }
+      } else {
+      uint8_t* hBn = nbuf ? hB1 : hB0;
       if (tid == 0) {
         mbar_arrive_expect_tx(&bars[1 + buf], (uint32_t)a.CL * a.slice);  // re-arm for step t+2
+        if (NCL > 1) mbar_arrive_expect_tx(&bars[3 + buf], (uint32_t)(NCL - 1) * a.CL * a.slice);
         fence_proxy_async_global();
-        bulk_g2s_multicast((nbuf ? hB1 : hB0) + me * a.slice, gst, a.slice, &bars[1 + nbuf], mask);
+        bulk_g2s_multicast(hBn + gq * a.slice, gst, a.slice, &bars[1 + nbuf], mask);
+        if (NCL > 1 && !a.mcrelw) {  // release the slice to the group's other clusters
+          if (a.mcfence) __threadfence();
+          st_release_gpu(a.xflags + (size_t)grp * NSL + gq, (uint32_t)(t + 1));
+        }
+      }
+      if (NCL > 1 && w == a.mcwarp) {
+        // Import the other clusters' slices at this CTA's position: lane c of warp
+        // 1 (not the MMA-issuing warp 0) pulls slice (c, me) of cluster c from L2
+        // and multicasts it to this cluster, all clusters in parallel.  Double-
+        // buffered staging is safe: the writer of step t+3 has consumed h_{t+2},
+        // which needs every importer's step t+1.
+        uint32_t* fl = a.xflags + (size_t)grp * NSL;
+        if (a.mcrelw && l == 0) {  // the release (it waits for the slice stores) off the MMA-issuing warp
+          if (a.mcfence) __threadfence();
+          st_release_gpu(fl + gq, (uint32_t)(t + 1));
+        }
+        __syncwarp();
+        for (int c = l; c < NCL; c += 32) {
+          if (c == cl) continue;
+          const int q = c * a.CL + (int)me;
+          if (a.mcpoll) spin_until_geq_relaxed(fl + q, (uint32_t)(t + 1));
+          else spin_until_geq(fl + q, (uint32_t)(t + 1));
+          if (a.prof && c == (cl == 0 ? 1 : 0) && t + 1 < a.prof_steps)  // remote flag seen (step t+1's data)
+            a.prof[((size_t)blockIdx.x * a.prof_steps + (t + 1)) * 8 + 6] = clock64();
+          fence_proxy_async_global();
+          const uint8_t* rsrc =
+              reinterpret_cast<const uint8_t*>(a.xstage) + (((size_t)grp * 2 + nbuf) * NSL + q) * a.slice;
+          bulk_g2s_multicast(hBn + q * a.slice, rsrc, a.slice, &bars[3 + nbuf], mask);
+        }
+        __syncwarp();
+      }
       }
     }
     FRNN_PROF(4, t);
@@ -1209,11 +1318,12 @@ bool gru_compact(const Problem& p) {
 }  // namespace
 
 // ---------------------------------------------------------------- host ----
-ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
+ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int ncl) {
   ClusterShape s{};
   const int NGP = ngp_of(p.NG);
   s.UPC = UPC;
-  s.CL = p.DH / UPC;
+  s.NCL = backward ? 1 : std::max(1, ncl);
+  s.CL = p.DH / (UPC * s.NCL);
   const int rows = UPC * NGP;
   s.R1 = rows < 128 ? rows : 128;
   s.R2 = rows - s.R1;
@@ -1229,13 +1339,27 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward) {
   s.threads = (int)align_up(pairs, 128);
   s.EPT = pairs <= MAXT ? 1 : 0;  // one unit pair per thread (0 = unsupported)
   if (!backward) {
-    s.acc1 = (uint32_t)align_up(s.K / 2, 32);
+    // One M=128 block whose K/2 TMEM columns + two accumulators exceed TMEM
+    // (DH > 960): the tail of K moves to an SMEM M=128 tile with its own
+    // accumulator, sized so the two operand paths take about equally long
+    // (TMEM-A ~50, SMEM-A M=128 ~90 cycles per K=16 step at N=16, DESIGN 4).
+    s.Ks = 0;
+    if (s.R2 == 0 && (int)align_up(s.K / 2, 32) + 2 * N > 512) {
+      const int nk = s.K / 16;
+      int nts = (nk * 90 + 139) / 140;
+      const char* kt = getenv("FRNN_FWD_KT");  // A/B hook: TMEM K columns of the split
+      if (kt) nts = atoi(kt) / 16;
+      nts = std::max(nk / 2, std::min(nts, (512 - 2 * N) / 8));
+      s.Ks = s.K - 16 * nts;
+    }
+    s.acc1 = (uint32_t)align_up((s.K - s.Ks) / 2, 32);
     s.acc2 = s.acc1 + N;
     s.tmem_cols = pow2_cols(s.acc2 + N);
-    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : 0) + (size_t)N * xs_pitch(rows) * 4 +
-             align_up(s.slice, 16) + 64;
+    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : (size_t)128 * s.Ks * 2) +
+             (size_t)N * xs_pitch(rows) * 4 + align_up(s.slice, 16) + 64;
     // (x and the trace move by per-thread loads/stores: TMA tiles measured slower)
-    s.ws = align_up((size_t)s.groups * 2 * s.CL * s.slice, 256);
+    s.ws = align_up((size_t)s.groups * 2 * s.NCL * s.CL * s.slice, 256);
+    if (s.NCL > 1) s.ws += align_up(sizeof(uint32_t) * s.groups * s.NCL * s.CL, 256);  // release flags
   } else {
     // R_p^T column blocks: MBT of 128 columns with A in TMEM, then MS of SSM
     // columns with A in SMEM, issued as pairs (TMEM block i interleaved with
@@ -1287,10 +1411,23 @@ bool cluster_ept_supported(int ept) { return ept == 1; }
 
 namespace {
 
+// Clusters per group of a forward plan (ctas_per_group = NCL x cluster).
+int plan_ncl(const Plan& pl) { return pl.cluster > 0 ? std::max(1, pl.ctas_per_group / pl.cluster) : 1; }
+
 CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, ClusterShape& cs) {
   const int N = pl.batch_tile;
-  cs = cluster_shape(p, pl.units_per_cta, N, backward);
+  cs = cluster_shape(p, pl.units_per_cta, N, backward, plan_ncl(pl));
   CArgs a{};
+  a.NCL = cs.NCL;
+  a.Ks = cs.Ks;
+  // (the slice writers' stores reach the flag's release through bar.sync; a full
+  // fence before it measured 0.47 us/step slower at H=1024 and is not needed)
+  a.mcfence = getenv("FRNN_MC_FENCE") ? atoi(getenv("FRNN_MC_FENCE")) : 0;
+  a.mcpoll = getenv("FRNN_MC_POLL") ? atoi(getenv("FRNN_MC_POLL")) : 0;
+  a.mcwarp = getenv("FRNN_MC_WARP") ? atoi(getenv("FRNN_MC_WARP")) : 1;
+  // own-cluster K range first: slower while the TMEM/SMEM split is not balanced per range (4.40 vs 4.09 us/step)
+  a.mclocal = getenv("FRNN_MC_LOCAL") ? atoi(getenv("FRNN_MC_LOCAL")) : 0;
+  a.mcrelw = getenv("FRNN_MC_RELW") ? atoi(getenv("FRNN_MC_RELW")) : 1;
   a.p = p;
   a.UPC = cs.UPC;
   a.CL = cs.CL;
@@ -1338,6 +1475,8 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   char* w = static_cast<char*>(ws);
   if (!backward) {
     a.xstage = reinterpret_cast<bf16*>(w);
+    if (cs.NCL > 1)
+      a.xflags = reinterpret_cast<uint32_t*>(w + align_up((size_t)cs.groups * 2 * cs.NCL * cs.CL * cs.slice, 256));
   } else {
     a.pstage = reinterpret_cast<float*>(w);
     size_t off = cs.ws;
@@ -1400,22 +1539,24 @@ KernelFn bwd_kernel(int L) {
   }
 }
 
+template <int V>
+KernelFn fwd_kernel(bool mc) {
+  return mc ? cl_fwd_kernel<V, 16, 1> : cl_fwd_kernel<V, 16, 0>;
+}
+
 template <bool BWD>
 cudaError_t launch_variant(int variant, const CArgs& a, const ClusterShape& cs, cudaStream_t s) {
-  const int grid = cs.groups * cs.CL;
+  const int grid = cs.groups * cs.NCL * cs.CL;
   const int fx = !BWD ? 0 : bwd_fixed_layout(a, cs) ? 1 : bwd_lean_layout(a) ? (bwd_plain(a) ? 3 : 2) : 0;
-  using K = KernelFn;
+  const bool mc = a.NCL > 1 || a.Ks > 0;
+  KernelFn k;
   switch (variant) {
-    case kElman:
-      return cluster_launch(BWD ? (K)bwd_kernel<kElman>(fx) : cl_fwd_kernel<kElman, 16>, a, grid, cs.threads, cs.smem, s);
-    case kLstm:
-      return cluster_launch(BWD ? (K)bwd_kernel<kLstm>(fx) : cl_fwd_kernel<kLstm, 16>, a, grid, cs.threads, cs.smem, s);
-    case kGru:
-      return cluster_launch(BWD ? (K)bwd_kernel<kGru>(fx) : cl_fwd_kernel<kGru, 16>, a, grid, cs.threads, cs.smem, s);
-    default:
-      return cluster_launch(BWD ? (K)bwd_kernel<kSlstm>(fx) : cl_fwd_kernel<kSlstm, 16>, a, grid, cs.threads, cs.smem,
-                            s);
+    case kElman: k = BWD ? bwd_kernel<kElman>(fx) : fwd_kernel<kElman>(mc); break;
+    case kLstm: k = BWD ? bwd_kernel<kLstm>(fx) : fwd_kernel<kLstm>(mc); break;
+    case kGru: k = BWD ? bwd_kernel<kGru>(fx) : fwd_kernel<kGru>(mc); break;
+    default: k = BWD ? bwd_kernel<kSlstm>(fx) : fwd_kernel<kSlstm>(mc); break;
   }
+  return cluster_launch(k, a, grid, cs.threads, cs.smem, s);
 }
 
 }  // namespace
@@ -1423,10 +1564,10 @@ cudaError_t launch_variant(int variant, const CArgs& a, const ClusterShape& cs, 
 bool cluster_kernel_attrs(int variant, bool backward, int* regs, int* local_bytes, int* max_threads) {
   const void* f;
   switch (variant) {
-    case kElman: f = backward ? (const void*)cl_bwd_kernel<kElman, 16, 0> : (const void*)cl_fwd_kernel<kElman, 16>; break;
-    case kLstm: f = backward ? (const void*)cl_bwd_kernel<kLstm, 16, 0> : (const void*)cl_fwd_kernel<kLstm, 16>; break;
-    case kGru: f = backward ? (const void*)cl_bwd_kernel<kGru, 16, 0> : (const void*)cl_fwd_kernel<kGru, 16>; break;
-    default: f = backward ? (const void*)cl_bwd_kernel<kSlstm, 16, 0> : (const void*)cl_fwd_kernel<kSlstm, 16>; break;
+    case kElman: f = backward ? (const void*)cl_bwd_kernel<kElman, 16, 0> : (const void*)cl_fwd_kernel<kElman, 16, 0>; break;
+    case kLstm: f = backward ? (const void*)cl_bwd_kernel<kLstm, 16, 0> : (const void*)cl_fwd_kernel<kLstm, 16, 0>; break;
+    case kGru: f = backward ? (const void*)cl_bwd_kernel<kGru, 16, 0> : (const void*)cl_fwd_kernel<kGru, 16, 0>; break;
+    default: f = backward ? (const void*)cl_bwd_kernel<kSlstm, 16, 0> : (const void*)cl_fwd_kernel<kSlstm, 16, 0>; break;
   }
   cudaFuncAttributes at{};
   if (cudaFuncGetAttributes(&at, f) != cudaSuccess) {
@@ -1440,7 +1581,39 @@ bool cluster_kernel_attrs(int variant, bool backward, int* regs, int* local_byte
 }
 
 size_t cluster_forward_ws(const Problem& p, const Plan& pl) {
-  return cluster_shape(p, pl.units_per_cta, pl.batch_tile, false).ws;
+  return cluster_shape(p, pl.units_per_cta, pl.batch_tile, false, plan_ncl(pl)).ws;
+}
+
+int cluster_forward_max_active(const Problem& p, const ClusterShape& cs) {
+  const void* f;
+  switch (p.variant) {
+    case kElman: f = (const void*)cl_fwd_kernel<kElman, 16, 1>; break;
+    case kLstm: f = (const void*)cl_fwd_kernel<kLstm, 16, 1>; break;
+    case kGru: f = (const void*)cl_fwd_kernel<kGru, 16, 1>; break;
+    default: f = (const void*)cl_fwd_kernel<kSlstm, 16, 1>; break;
+  }
+  if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs.smem) != cudaSuccess ||
+      (cs.CL > 8 && cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs.CL * cs.NCL * cs.groups);
+  cfg.blockDim = dim3(cs.threads);
+  cfg.dynamicSmemBytes = cs.smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs.CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, f, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 size_t cluster_backward_ws(const Problem& p, const Plan& pl) {
@@ -1455,6 +1628,10 @@ size_t cluster_backward_ws(const Problem& p, const Plan& pl) {
 cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s) {
   ClusterShape cs;
   CArgs a = make_cargs(p, pl, ws, false, cs);
+  if (a.xflags) {
+    cudaError_t e = cudaMemsetAsync(a.xflags, 0, sizeof(uint32_t) * cs.groups * cs.NCL * cs.CL, s);
+    if (e != cudaSuccess) return e;
+  }
   kt_begin(KT_FWD, s);
   cudaError_t e = launch_variant<false>(p.variant, a, cs, s);
   kt_end(KT_FWD, s);

@@ -243,6 +243,53 @@ bool plan_cluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out
   return false;
 }
 
+// Forward heads whose R does not fit one cluster (4-gate DH > 768): the group's
+// units over NCL clusters of CL CTAs (fused_cluster.cu, NCL > 1) -- R stays
+// resident in TMEM + SMEM, h slices cross clusters through L2 with release
+// flags.  Fewest clusters first (every extra cluster is another L2 round trip
+// per step), then the largest cluster; all NCL * groups clusters must be
+// co-resident (the kernel spins on the other clusters' flags).
+bool plan_multicluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
+  if (pass != 0 || getenv("FRNN_NO_MULTICLUSTER")) {
+    *why = "multi-cluster: forward only";
+    return false;
+  }
+  const int NGP = ngp_of(p.NG), N = 16;
+  for (int ncl = 2; ncl <= 9; ++ncl)
+    for (int CL = lim.cluster_max; CL >= 2; --CL) {
+      if (p.DH % (ncl * CL)) continue;
+      const int upc = p.DH / (ncl * CL);
+      // (UPC % 8: a slice is whole 8-wide K core-matrix columns of the h tile)
+      if (upc % 8 || upc * NGP > 128 || upc / 2 * N > 384) continue;
+      if ((CL * upc) % 16) continue;  // whole 16-wide K steps per cluster (local range issued first)
+      const ClusterShape cs = cluster_shape(p, upc, N, false, ncl);
+      if ((int)cs.smem > lim.smem_optin || (int)cs.tmem_cols > lim.tmem_cols || !cluster_ept_supported(cs.EPT))
+        continue;
+      if ((cs.K - cs.Ks) % 16 || cs.Ks % 16) continue;
+      const int active = cluster_forward_max_active(p, cs);
+      if (active > 0 && active < ncl * cs.groups) continue;  // (no device: assume co-resident)
+      if (active == 0 && ncl * cs.groups * CL > lim.sm_count) continue;
+      Plan& pl = *out;
+      pl = Plan{};
+      pl.algo = FRNN_ALGO_FUSED;
+      pl.cluster = CL;
+      pl.rows_per_cta = upc * NGP;
+      pl.batch_tile = N;
+      pl.units_per_cta = upc;
+      pl.ctas_per_group = ncl * CL;
+      pl.groups = cs.groups;
+      pl.grid = cs.groups * ncl * CL;
+      pl.threads = cs.threads;
+      pl.smem_bytes = (int)cs.smem;
+      pl.tmem_cols = (int)cs.tmem_cols;
+      pl.k_split = 1;
+      pl.ws_bytes = cluster_forward_ws(p, pl);
+      return true;
+    }
+  *why = "multi-cluster: no NCL x CL x UPC split of the head fits";
+  return false;
+}
+
 bool plan_alt(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
   if (!alt_supported(p, why)) return false;
   const auto sol = run(alt_csp(p, pass, lim));
@@ -412,6 +459,8 @@ int solve_plan(const Problem& p, int pass, int algo, const DeviceLimits& lim, Pl
   std::string w1, w2, w3;
   if (algo == FRNN_ALGO_AUTO || algo == FRNN_ALGO_FUSED) {
     if (plan_cluster(p, pass, lim, out, &w1)) return FRNN_OK;
+    std::string w4;
+    if (plan_multicluster(p, pass, lim, out, &w4)) return FRNN_OK;
     if (plan_fused(p, pass, lim, out, &w2)) return FRNN_OK;
     if (algo == FRNN_ALGO_FUSED) {
       *why = w1 + "; " + w2;

@@ -335,6 +335,46 @@ __device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t
     mma1_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, b0 + (uint64_t)k * b_step, id1, id2,
                k > 0 || acc0);
 }
+// Whole warp.  One block of R rows whose K is split between TMEM (nts steps)
+// and SMEM (nss <= nts steps, M=128 SS form), two accumulators:
+//   D1 (+)= sum_{k<nts} A_tmem(ta + 8k) . B(b0 + k*bk)
+//   D2 (+)= sum_{k<nss} A_smem(a2 + k*a2k) . B(b0 + (nts+k)*bk)
+// issued interleaved so that the TMEM-A and SMEM-A operand paths overlap.
+__device__ __forceinline__ void mma_ksplit(uint32_t d1, uint32_t ta, int nts, uint32_t d2, uint64_t a2, uint64_t a2k,
+                                           int nss, uint64_t b0, uint64_t bk, uint32_t idesc) {
+  const uint64_t b2 = b0 + (uint64_t)nts * bk;
+  int k = 0;
+  for (; k < nss; ++k) {
+    mma1_ts(d1, ta + 8u * k, b0 + (uint64_t)k * bk, idesc, k > 0);
+    mma1_ss(d2, a2 + (uint64_t)k * a2k, b2 + (uint64_t)k * bk, idesc, k > 0);
+  }
+  for (; k < nts; ++k) mma1_ts(d1, ta + 8u * k, b0 + (uint64_t)k * bk, idesc, k > 0);
+}
+// Whole warp, one PTX loop on uniform registers (no per-MMA elect waterfall).
+// Interleaves n1 TMEM-A steps  D1 (+)= A_tmem(ta + 8i) . B(b1 + i*bk)
+// with        n2 SMEM-A steps  D2 (+)= A_smem(a2 + i*a2k) . B(b2 + i*bk);
+// accumulate = (i > 0) || acc1 (resp. acc2).
+__device__ __forceinline__ void mma_chain_ksplit(uint32_t d1, uint32_t ta, uint64_t b1, int n1, uint32_t acc1,
+                                                 uint32_t d2, uint64_t a2, uint64_t a2k, uint64_t b2, int n2,
+                                                 uint32_t acc2, uint64_t bk, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, q, r, s, g, h, p1, p2, z1, z2;\n\t.reg .b32 k, ta, n;\n\t.reg .b64 bb1, aa2, bb2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 k, 0;\n\tmov.b32 ta, %1;\n\tmov.b64 bb1, %2;\n\tmov.b64 aa2, %6;\n\tmov.b64 bb2, %8;\n\t"
+      "max.s32 n, %3, %9;\n\tsetp.ne.b32 z1, %4, 0;\n\tsetp.ne.b32 z2, %10, 0;\n\t"
+      "setp.ge.s32 q, k, n;\n\t@q bra.uni KS_END%=;\n\t"
+      "KS_LOOP%=:\n\t"
+      "setp.lt.s32 r, k, %3;\n\tsetp.lt.s32 s, k, %9;\n\tand.pred g, e, r;\n\tand.pred h, e, s;\n\t"
+      "setp.ne.or.b32 p1, k, 0, z1;\n\tsetp.ne.or.b32 p2, k, 0, z2;\n\t"
+      "@g tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bb1, %12, p1;\n\t"
+      "@h tcgen05.mma.cta_group::1.kind::f16 [%5], aa2, bb2, %12, p2;\n\t"
+      "add.u32 ta, ta, 8;\n\tadd.u64 bb1, bb1, %11;\n\tadd.u64 aa2, aa2, %7;\n\tadd.u64 bb2, bb2, %11;\n\t"
+      "add.s32 k, k, 1;\n\tsetp.lt.s32 q, k, n;\n\t@q bra.uni KS_LOOP%=;\n\t"
+      "KS_END%=:\n\t}" ::"r"(d1),
+      "r"(ta), "l"(b1), "r"(n1), "r"(acc1), "r"(d2), "l"(a2), "l"(a2k), "l"(b2), "r"(n2), "r"(acc2), "l"(bk),
+      "r"(idesc)
+      : "memory");
+}
 // 12-step blocks: a whole K=192 backward block (UPC=48, 4-gate cells) per asm.
 __device__ __forceinline__ void mma12_ts_ss(uint32_t d1, uint32_t ta, uint32_t d2, uint64_t ad, uint64_t ak,
                                             uint64_t bd, uint64_t bk, uint32_t id1, uint32_t id2, uint32_t acc) {
@@ -613,6 +653,9 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -633,6 +676,22 @@ __device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t targe
       else if (now - t0 > 4000000000ull) __trap();
     }
   }
+}
+
+// Spin with relaxed loads (no L1 invalidate per probe), then one acquire.
+__device__ __forceinline__ void spin_until_geq_relaxed(const uint32_t* p, uint32_t target) {
+  uint64_t t0 = 0;
+  uint32_t n = 0, v;
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) break;
+    if ((++n & 4095u) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) __trap();
+    }
+  }
+  (void)ld_acquire(p);
 }
 
 // L2-only 16-byte load (data written by other SMs during this launch).

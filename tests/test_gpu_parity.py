@@ -194,9 +194,24 @@ def test_bf16_cluster_three_batch_tiles(eng, orc, v):
                                        ("elman", 1, 512, 16), ("gru", 1, 512, 16)])
 def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
     """Head dims whose tilings differ from the headline: DH=640 (UPC=40, five
-    TMEM blocks, no SMEM block), DH=896 (no cluster tiling: L2-flag fused
+    TMEM blocks, no SMEM block), DH=896 (no single-cluster tiling: two-cluster
     forward + alternating backward), two heads of 384, Elman 512."""
     inp = orc.generate(v, 6, B, NH, DH, seed=13)
+    check_bf16(eng, orc, v, inp)
+
+
+@pytest.mark.parametrize("v,NH,DH,B,ncl", [("lstm", 1, 1024, 16, 2), ("slstm", 1, 1024, 20, 2),
+                                           ("gru", 1, 1152, 16, 3), ("elman", 1, 1024, 8, 2),
+                                           ("slstm", 2, 896, 16, 2)])
+def test_bf16_multicluster_forward(eng, orc, v, NH, DH, B, ncl):
+    """R-resident forward beyond one cluster (fused_cluster.cu, NCL > 1): the
+    head's units over NCL clusters, h slices of the other clusters imported
+    through L2 behind release flags; DH > 960 also splits each CTA's R rows
+    along K between TMEM and an SMEM M=128 tile (two accumulators).  B=20: two
+    batch tiles (four clusters); NH=2: two heads.  Backward: alternating."""
+    pf = eng.plan(v, 6, B, NH, DH, "bf16", "forward")
+    assert pf["algo"] == 1 and pf["ctas_per_group"] == ncl * pf["cluster"], pf
+    inp = orc.generate(v, 6, B, NH, DH, seed=21)
     check_bf16(eng, orc, v, inp)
 
 
