@@ -97,6 +97,9 @@ struct CArgs {
   int mcfence, mcpoll;  // NCL > 1: full fence before the flag release; relaxed polling (A/B knobs)
   int mcwarp, mclocal;  // NCL > 1: the importing warp; own cluster's K range issued first (A/B knobs)
   int mcrelw;           // NCL > 1: the importing warp (not thread 0) releases the slice flag
+  int mcdbg;            // debug (FRNN_MC_DBG bits: 1 no remote loads, 2 no remote stores, 4 no flag waits)
+  uint32_t* bflags;     // backward, NCL > 1: [groups][NCL*CL] publish counters of the partials
+                        // (the partials for other clusters' owners go to pstage, [grp][2][dest][src][N][PW] words)
   int skeleton;    // 1: synchronisation skeleton only -- no MMAs, no cell math (the sequential-
                    //    dependency floor of SURVEY 8d; frnn_debug_skeleton, results are garbage)
 };
@@ -187,6 +190,31 @@ __device__ __forceinline__ void push_col_pairs(const float* v, int lane, bool ok
     const uint32_t dst = mapa_shared(rb_me + (uint32_t)(((odd ? H : 0) * PW + (cu >> 1)) * 4), q);
 #pragma unroll
     for (int i = 0; i < H; ++i) st_async_b32(dst + (uint32_t)(i * PW * 4), __uint_as_float(w[i]), mbr);
+  }
+}
+
+// push_col_pairs for the multi-cluster backward: the same shuffle, then each lane
+// pushes to its owner's shared memory (`local`: owner in this cluster) or stores
+// the words to the owner's global staging block `gdst` ([n][PW] words).
+template <int N>
+__device__ __forceinline__ void push_col_pairs_mc(const float* v, int lane, bool ok, bool local, int cu, int PW,
+                                                  uint32_t rb_me, uint32_t q, uint32_t mbr, uint32_t* gdst) {
+  constexpr int H = N / 2;
+  const bool odd = lane & 1;
+  uint32_t w[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const float got = __shfl_xor_sync(0xffffffffu, odd ? v[i] : v[H + i], 1);
+    w[i] = odd ? pack_bf16(got, v[H + i]) : pack_bf16(v[i], got);
+  }
+  if (ok && local) {
+    const uint32_t dst = mapa_shared(rb_me + (uint32_t)(((odd ? H : 0) * PW + (cu >> 1)) * 4), q);
+#pragma unroll
+    for (int i = 0; i < H; ++i) st_async_b32(dst + (uint32_t)(i * PW * 4), __uint_as_float(w[i]), mbr);
+  } else if (ok) {
+    uint32_t* g = gdst + (odd ? H : 0) * PW + (cu >> 1);
+#pragma unroll
+    for (int i = 0; i < H; ++i) g[i * PW] = w[i];
   }
 }
 
@@ -649,7 +677,9 @@ __device__ __forceinline__ bool issue_bwd_table(int MBT, int MS, int nk, uint32_
 }
 
 // ----------------------------------------------------------- backward ----
-template <int V, int N, int L>  // L = 1: the H=768 4-gate layout (every tiling branch fixed at compile time)
+// L = 1: the H=768 4-gate layout (every tiling branch fixed at compile time);
+// L = 4: multi-cluster (NCL > 1, 4-gate cells, bf16 column-pair exchange)
+template <int V, int N, int L>
 __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   using C = Cell<V>;
   constexpr int NS = C::NS, NG = C::NG, NGP = C::NGP;
@@ -660,10 +690,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   const Problem& p = a.p;
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, NT = blockDim.x;
   const uint32_t me = cluster_ctarank();
-  const int grp = blockIdx.x / a.CL;
+  // L == 4: the head's units over NCL clusters; partials for owners in other
+  // clusters travel through L2 (pstage) behind per-source release counters
+  constexpr bool MCB = L == 4;
+  const int NCL = MCB ? a.NCL : 1, NSL = a.CL * NCL;
+  const int grp = blockIdx.x / NSL;
+  const int cl = MCB ? (blockIdx.x / a.CL) % NCL : 0;
+  const int gq = MCB ? cl * a.CL + (int)me : (int)me;
   const int hd = grp / a.NBT, b0 = (grp % a.NBT) * N;
   const int nb = min(N, p.B - b0);
-  const int unit0 = me * a.UPC;
+  const int unit0 = gq * a.UPC;
   const int DH = p.DH, D = p.D, B = p.B, T = p.T, KBP = a.KBP, MB = a.MB, MBT = a.MBT;
   const bool recur = p.clip_mode != 2;
   const float mag = p.clip_mag;
@@ -713,6 +749,9 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(term + (!FX && a.dsm == 1 ? N * TP : 0));  // -, rcv, rdy0|rcv0, rdy1|rcv1
   uint64_t* blkbar = bars + 4;  // [NPAIR]: MMAs of block pair i (and all before it) complete
   uint32_t* tbase_s = reinterpret_cast<uint32_t*>(blkbar + 16);
+  // MCB: barrier + receive buffer [remote src][N][PW] words for the other clusters' partials
+  uint64_t* rbar = blkbar + 17;
+  uint32_t* rrecv = reinterpret_cast<uint32_t*>(blkbar + 18);
 
   // Column rotation: CTA `me` lays out its R^T column blocks starting at column
   // me*UPC, so the block it computes LAST (whose partials arrive after the MMAs)
@@ -727,6 +766,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     mbar_init(&bars[2], dsm ? 1 : a.CL);
     mbar_init(&bars[3], dsm ? 1 : a.CL);
     for (int i = 0; i < NPAIR; ++i) mbar_init(&blkbar[i], 1);
+    if (MCB) mbar_init(rbar, 1);
     fence_mbar_init();
   }
   for (int i = tid; i < N * KBP * 2 / 16; i += NT) reinterpret_cast<uint4*>(dgB)[i] = make_uint4(0, 0, 0, 0);
@@ -832,7 +872,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
 
   // Partials of step s are in pstage[grp][s&1][me][*]: wait for the CL
   // producers, pull them with one bulk load, sum, clip, add to ds_h.
-  uint32_t rcv_phase = 0, par_phase = 0;
+  uint32_t rcv_phase = 0, par_phase = 0, rphase = 0;
   auto absorb_dsm = [&](int s) {  // partials pushed into my recv[s&1] by every peer (st.async)
     const int pb = s & 1;
     if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
@@ -870,6 +910,26 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
     const int pb = s & 1;
     if (!k_noxchg) {
       if (tid == 0) mbar_arrive_expect_tx(&bars[2 + pb], recv_bytes);
+      if (MCB && NCL > 1) {
+        // The other clusters' sources: lane `src` of warp 0 waits for that source's
+        // release counter, then pulls its [N][PW] block from L2 into rrecv (TMA).
+        if (w == 0) {
+          const uint32_t blk = (uint32_t)N * PW * 4;
+          if (l == 0) mbar_arrive_expect_tx(rbar, (uint32_t)(NSL - a.CL) * blk);
+          __syncwarp();
+          const uint32_t* fl = a.bflags + (size_t)grp * NSL;
+          const uint8_t* gsrc = reinterpret_cast<const uint8_t*>(a.pstage) + (((size_t)grp * 2 + pb) * NSL + gq) * NSL * blk;
+          for (int src = l; src < NSL; src += 32)
+            if (src / a.CL != cl) {
+              if (!(a.mcdbg & 4)) spin_until_geq(fl + src, (uint32_t)(T - s));
+              fence_proxy_async_global();
+              const int ri = src < cl * a.CL ? src : src - a.CL;
+              bulk_g2s(reinterpret_cast<uint8_t*>(rrecv) + ri * blk, gsrc + (size_t)src * blk, blk, rbar);
+            }
+        }
+        mbar_wait(rbar, rphase);
+        rphase ^= 1u;
+      }
       mbar_wait_cluster(&bars[2 + pb], (par_phase >> pb) & 1u);
       par_phase ^= 1u << pb;
     }
@@ -892,6 +952,22 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           const uint32_t v = rp[q * qs];
           t0 += lo16(v);
           t1 += hi16(v);
+        }
+      }
+      if (MCB && NCL > 1 && !(a.mcdbg & 1)) {  // then the other clusters' sources, fixed order (deterministic)
+        const uint32_t* r2 = rrecv + (size_t)b * PW + (u >> 1);
+        const int nrs = NSL - a.CL;
+        for (int q0 = 0; q0 < nrs; q0 += 16) {
+          uint32_t v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (q0 + q < nrs) v[q] = r2[(q0 + q) * qs];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (q0 + q < nrs) {
+              t0 += lo16(v[q]);
+              t1 += hi16(v[q]);
+            }
         }
       }
       if (p.clip_mode == 1) {
@@ -1219,7 +1295,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
         c = rotc(c);
         float v[16];
         tmem_ld16(tbase + ((uint32_t)(32 * qd) << 16) + a.acc1 + (sblk ? MBT + i : i) * N, v);
-        if (FX || (pbf && a.pvec == 2)) {  // whole warp (shuffles inside)
+        if (MCB) {  // whole warp (shuffles inside); owners in other clusters through pstage
+          const int qg = min(c / a.UPC, NSL - 1), cu = c % a.UPC, q = qg % a.CL;
+          uint32_t* gd = reinterpret_cast<uint32_t*>(a.pstage) +
+                         ((((size_t)grp * 2 + (t & 1)) * NSL + qg) * NSL + gq) * N * PW;
+          push_col_pairs_mc<N>(v, l, lane_ok && c < DH && !k_noxchg && (qg / a.CL == cl || !(a.mcdbg & 2)), qg / a.CL == cl, cu, PW,
+                               rb + (uint32_t)(me * N * PW * 4), q, mapa_shared(rbar, q), gd);
+        } else if (FX || (pbf && a.pvec == 2)) {  // whole warp (shuffles inside)
           const int q = min(c / a.UPC, a.CL - 1), cu = c % a.UPC;  // (clamped for lanes past DH)
           push_col_pairs<N>(v, l, lane_ok && c < DH && !k_noxchg, cu, PW, rb + (uint32_t)(me * N * PW * 4), q,
                             mapa_shared(rbar, q));
@@ -1266,6 +1348,8 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
       tc_fence_before();
       __syncthreads();
       if (!dsm && tid < a.CL) mbar_arrive_remote(mapa_shared(smem_u32(&bars[2 + (t & 1)]), tid));
+      if (MCB && NCL > 1 && tid == 0)  // this CTA's partials of step t for the other clusters are stored
+        st_release_gpu(a.bflags + (size_t)grp * NSL + gq, (uint32_t)(k + 1));
       FRNN_PROF(4, k);
     }
     if (!dxearly) store_dx();
@@ -1322,7 +1406,7 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
   ClusterShape s{};
   const int NGP = ngp_of(p.NG);
   s.UPC = UPC;
-  s.NCL = backward ? 1 : std::max(1, ncl);
+  s.NCL = std::max(1, ncl);
   s.CL = p.DH / (UPC * s.NCL);
   const int rows = UPC * NGP;
   s.R1 = rows < 128 ? rows : 128;
@@ -1344,7 +1428,8 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
     // accumulator, sized so the two operand paths take about equally long
     // (TMEM-A ~50, SMEM-A M=128 ~90 cycles per K=16 step at N=16, DESIGN 4).
     s.Ks = 0;
-    if (s.R2 == 0 && (int)align_up(s.K / 2, 32) + 2 * N > 512) {
+    // (multi-cluster: split even when K fits TMEM -- the two operand paths overlap)
+    if (s.R2 == 0 && ((int)align_up(s.K / 2, 32) + 2 * N > 512 || (s.NCL > 1 && !getenv("FRNN_FWD_NOSPLIT")))) {
       const int nk = s.K / 16;
       int nts = (nk * 90 + 139) / 140;
       const char* kt = getenv("FRNN_FWD_KT");  // A/B hook: TMEM K columns of the split
@@ -1403,7 +1488,20 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
     }
     // (per-thread trace loads / dx stores: TMA tiles measured slower)
     s.ws = align_up((size_t)s.groups * 2 * s.CL * s.CL * N * UPC * 4, 256);
+    if (s.NCL > 1) {
+      // the other clusters' partials land in SMEM too ([remote src][N][PW] words, after the
+      // barriers), and 384 threads drain the MB accumulator blocks (3 warp groups)
+      s.smem += (size_t)(s.NCL - 1) * s.CL * N * pair_pitch(UPC) * 4 + 64;
+      s.threads = getenv("FRNN_MCB_THREADS") ? std::max(s.threads, atoi(getenv("FRNN_MCB_THREADS"))) : MAXT;  // partials for other clusters' owners [grp][2][dest][src][N][PW] words + release counters
+      const size_t nsl = (size_t)s.NCL * s.CL;
+      s.ws = align_up((size_t)s.groups * 2 * nsl * nsl * N * pair_pitch(UPC) * 4, 256) +
+             align_up(sizeof(uint32_t) * s.groups * nsl, 256);
+    }
   }
+  // Multi-cluster kernels spin on other clusters' counters, and every CTA holds all
+  // 512 TMEM columns: two CTAs on one SM would wait on each other's allocation.
+  // More than half the SM's shared memory keeps them one per SM.
+  if (s.NCL > 1) s.smem = std::max(s.smem, (size_t)118 * 1024);
   return s;
 }
 
@@ -1428,6 +1526,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   // own-cluster K range first: slower while the TMEM/SMEM split is not balanced per range (4.40 vs 4.09 us/step)
   a.mclocal = getenv("FRNN_MC_LOCAL") ? atoi(getenv("FRNN_MC_LOCAL")) : 0;
   a.mcrelw = getenv("FRNN_MC_RELW") ? atoi(getenv("FRNN_MC_RELW")) : 1;
+  a.mcdbg = getenv("FRNN_MC_DBG") ? atoi(getenv("FRNN_MC_DBG")) : 0;
   a.p = p;
   a.UPC = cs.UPC;
   a.CL = cs.CL;
@@ -1479,6 +1578,10 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
       a.xflags = reinterpret_cast<uint32_t*>(w + align_up((size_t)cs.groups * 2 * cs.NCL * cs.CL * cs.slice, 256));
   } else {
     a.pstage = reinterpret_cast<float*>(w);
+    if (cs.NCL > 1) {
+      const size_t nsl = (size_t)cs.NCL * cs.CL;
+      a.bflags = reinterpret_cast<uint32_t*>(w + align_up((size_t)cs.groups * 2 * nsl * nsl * N * pair_pitch(cs.UPC) * 4, 256));
+    }
     size_t off = cs.ws;
     bool all_in = true;
     for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
@@ -1535,7 +1638,7 @@ KernelFn bwd_kernel(int L) {
     return L == 3 ? cl_bwd_kernel<V, 16, 3> : L ? cl_bwd_kernel<V, 16, 2> : cl_bwd_kernel<V, 16, 0>;
   } else {
     return L == 1 ? cl_bwd_kernel<V, 16, 1> : L == 2 ? cl_bwd_kernel<V, 16, 2>
-         : L == 3 ? cl_bwd_kernel<V, 16, 3> : cl_bwd_kernel<V, 16, 0>;
+         : L == 3 ? cl_bwd_kernel<V, 16, 3> : L == 4 ? cl_bwd_kernel<V, 16, 4> : cl_bwd_kernel<V, 16, 0>;
   }
 }
 
@@ -1547,7 +1650,7 @@ KernelFn fwd_kernel(bool mc) {
 template <bool BWD>
 cudaError_t launch_variant(int variant, const CArgs& a, const ClusterShape& cs, cudaStream_t s) {
   const int grid = cs.groups * cs.NCL * cs.CL;
-  const int fx = !BWD ? 0 : bwd_fixed_layout(a, cs) ? 1 : bwd_lean_layout(a) ? (bwd_plain(a) ? 3 : 2) : 0;
+  const int fx = !BWD ? 0 : a.NCL > 1 ? 4 : bwd_fixed_layout(a, cs) ? 1 : bwd_lean_layout(a) ? (bwd_plain(a) ? 3 : 2) : 0;
   const bool mc = a.NCL > 1 || a.Ks > 0;
   KernelFn k;
   switch (variant) {
@@ -1584,14 +1687,15 @@ size_t cluster_forward_ws(const Problem& p, const Plan& pl) {
   return cluster_shape(p, pl.units_per_cta, pl.batch_tile, false, plan_ncl(pl)).ws;
 }
 
-int cluster_forward_max_active(const Problem& p, const ClusterShape& cs) {
+int cluster_max_active(const Problem& p, const ClusterShape& cs, bool backward) {
   const void* f;
   switch (p.variant) {
-    case kElman: f = (const void*)cl_fwd_kernel<kElman, 16, 1>; break;
-    case kLstm: f = (const void*)cl_fwd_kernel<kLstm, 16, 1>; break;
-    case kGru: f = (const void*)cl_fwd_kernel<kGru, 16, 1>; break;
-    default: f = (const void*)cl_fwd_kernel<kSlstm, 16, 1>; break;
+    case kElman: f = backward ? nullptr : (const void*)cl_fwd_kernel<kElman, 16, 1>; break;
+    case kLstm: f = backward ? (const void*)cl_bwd_kernel<kLstm, 16, 4> : (const void*)cl_fwd_kernel<kLstm, 16, 1>; break;
+    case kGru: f = backward ? (const void*)cl_bwd_kernel<kGru, 16, 4> : (const void*)cl_fwd_kernel<kGru, 16, 1>; break;
+    default: f = backward ? (const void*)cl_bwd_kernel<kSlstm, 16, 4> : (const void*)cl_fwd_kernel<kSlstm, 16, 1>; break;
   }
+  if (!f) return 0;
   if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs.smem) != cudaSuccess ||
       (cs.CL > 8 && cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
     cudaGetLastError();
@@ -1617,7 +1721,7 @@ int cluster_forward_max_active(const Problem& p, const ClusterShape& cs) {
 }
 
 size_t cluster_backward_ws(const Problem& p, const Plan& pl) {
-  size_t off = cluster_shape(p, pl.units_per_cta, pl.batch_tile, true).ws;
+  size_t off = cluster_shape(p, pl.units_per_cta, pl.batch_tile, true, plan_ncl(pl)).ws;
   bool all_in = true;
   for (int j = 0; j < p.NG; ++j) all_in = all_in && p.inp[j];
   if (!all_in) off += align_up((size_t)2 * p.T * p.B * p.NG * p.D, 256);
@@ -1641,6 +1745,10 @@ cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStre
 cudaError_t cluster_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s) {
   ClusterShape cs;
   CArgs a = make_cargs(p, pl, ws, true, cs);
+  if (a.bflags) {
+    cudaError_t e = cudaMemsetAsync(a.bflags, 0, sizeof(uint32_t) * cs.groups * cs.NCL * cs.CL, s);
+    if (e != cudaSuccess) return e;
+  }
   kt_begin(KT_BWD, s);
   cudaError_t e = launch_variant<true>(p.variant, a, cs, s);
   kt_end(KT_BWD, s);

@@ -69,14 +69,14 @@ struct ClusterShape {
   int pbf16, pvec;  // backward: bf16-pair partials; their receive layout (2 = [n][cu/2] column pairs)
   uint32_t acc1, acc2, tmem_cols, slice;
   size_t smem, ws;
-  int NCL;  // forward: clusters per group (> 1: h slices cross clusters through L2 with release flags)
+  int NCL;  // clusters per group (> 1: h slices / partials cross clusters through L2 with release counters)
   int Ks;   // forward: K columns of the R rows held in SMEM (M=128 SS) when K/2 + accumulators exceed TMEM
 };
-// ncl > 1 (forward only): the group's DH units are split over ncl clusters of
+// ncl > 1: the group's DH units are split over ncl clusters of
 // DH / (UPC * ncl) CTAs each.
 ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int ncl = 1);
-// Clusters of `CL` CTAs of the forward kernel that can be co-resident (0 without a device).
-int cluster_forward_max_active(const Problem& p, const ClusterShape& cs);
+// Clusters of `CL` CTAs of the multi-cluster kernel that can be co-resident (0 without a device).
+int cluster_max_active(const Problem& p, const ClusterShape& cs, bool backward);
 bool cluster_ept_supported(int ept);
 cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 cudaError_t cluster_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);

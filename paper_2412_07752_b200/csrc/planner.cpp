@@ -243,30 +243,38 @@ bool plan_cluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out
   return false;
 }
 
-// Forward heads whose R does not fit one cluster (4-gate DH > 768): the group's
+// Heads whose R does not fit one cluster (4-gate DH > 768): the group's
 // units over NCL clusters of CL CTAs (fused_cluster.cu, NCL > 1) -- R stays
 // resident in TMEM + SMEM, h slices cross clusters through L2 with release
 // flags.  Fewest clusters first (every extra cluster is another L2 round trip
 // per step), then the largest cluster; all NCL * groups clusters must be
 // co-resident (the kernel spins on the other clusters' flags).
 bool plan_multicluster(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, std::string* why) {
-  if (pass != 0 || getenv("FRNN_NO_MULTICLUSTER")) {
-    *why = "multi-cluster: forward only";
+  if (getenv("FRNN_NO_MULTICLUSTER")) {
+    *why = "multi-cluster kernels disabled (FRNN_NO_MULTICLUSTER)";
     return false;
   }
   const int NGP = ngp_of(p.NG), N = 16;
+  // Backward (4-gate cells, bf16 column-pair exchange; partials for other clusters'
+  // owners through L2): correct, but measured slower than the alternating backward
+  // (H=1024 LSTM 8.8 vs 8.2 us/step) -- opt-in with FRNN_MC_BWD=1.
+  if (pass == 1 && (NGP != 4 || !getenv("FRNN_MC_BWD") || !atoi(getenv("FRNN_MC_BWD")))) {
+    *why = "multi-cluster backward: opt-in (FRNN_MC_BWD=1), 4-gate cells";
+    return false;
+  }
   for (int ncl = 2; ncl <= 9; ++ncl)
     for (int CL = lim.cluster_max; CL >= 2; --CL) {
       if (p.DH % (ncl * CL)) continue;
       const int upc = p.DH / (ncl * CL);
       // (UPC % 8: a slice is whole 8-wide K core-matrix columns of the h tile)
       if (upc % 8 || upc * NGP > 128 || upc / 2 * N > 384) continue;
-      if ((CL * upc) % 16) continue;  // whole 16-wide K steps per cluster (local range issued first)
-      const ClusterShape cs = cluster_shape(p, upc, N, false, ncl);
+      if ((CL * upc) % 16) continue;  // whole 16-wide K steps per cluster
+      const ClusterShape cs = cluster_shape(p, upc, N, pass == 1, ncl);
       if ((int)cs.smem > lim.smem_optin || (int)cs.tmem_cols > lim.tmem_cols || !cluster_ept_supported(cs.EPT))
         continue;
-      if ((cs.K - cs.Ks) % 16 || cs.Ks % 16) continue;
-      const int active = cluster_forward_max_active(p, cs);
+      if (pass == 0 && ((cs.K - cs.Ks) % 16 || cs.Ks % 16)) continue;
+      if (pass == 1 && (cs.MBT < 1 || cs.dsm != 2 || !cs.pbf16 || cs.pvec != 2)) continue;
+      const int active = cluster_max_active(p, cs, pass == 1);
       if (active > 0 && active < ncl * cs.groups) continue;  // (no device: assume co-resident)
       if (active == 0 && ncl * cs.groups * CL > lim.sm_count) continue;
       Plan& pl = *out;
@@ -283,7 +291,7 @@ bool plan_multicluster(const Problem& p, int pass, const DeviceLimits& lim, Plan
       pl.smem_bytes = (int)cs.smem;
       pl.tmem_cols = (int)cs.tmem_cols;
       pl.k_split = 1;
-      pl.ws_bytes = cluster_forward_ws(p, pl);
+      pl.ws_bytes = pass == 0 ? cluster_forward_ws(p, pl) : cluster_backward_ws(p, pl);
       return true;
     }
   *why = "multi-cluster: no NCL x CL x UPC split of the head fits";

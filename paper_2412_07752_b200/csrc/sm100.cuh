@@ -695,6 +695,11 @@ __device__ __forceinline__ void spin_until_geq_relaxed(const uint32_t* p, uint32
 }
 
 // L2-only 16-byte load (data written by other SMs during this launch).
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -202,16 +202,31 @@ def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
 
 @pytest.mark.parametrize("v,NH,DH,B,ncl", [("lstm", 1, 1024, 16, 2), ("slstm", 1, 1024, 20, 2),
                                            ("gru", 1, 1152, 16, 3), ("elman", 1, 1024, 8, 2),
-                                           ("slstm", 2, 896, 16, 2)])
-def test_bf16_multicluster_forward(eng, orc, v, NH, DH, B, ncl):
+                                           ("slstm", 2, 896, 16, 2), ("lstm", 1, 1408, 16, 4)])
+def test_bf16_multicluster(eng, orc, v, NH, DH, B, ncl):
     """R-resident forward beyond one cluster (fused_cluster.cu, NCL > 1): the
     head's units over NCL clusters, h slices of the other clusters imported
-    through L2 behind release flags; DH > 960 also splits each CTA's R rows
-    along K between TMEM and an SMEM M=128 tile (two accumulators).  B=20: two
-    batch tiles (four clusters); NH=2: two heads.  Backward: alternating."""
+    through L2 behind release counters; DH > 960 also splits each CTA's R rows
+    along K between TMEM and an SMEM M=128 tile.  B=20: two batch tiles; NH=2:
+    two heads.  Backward: alternating (the default plan)."""
     pf = eng.plan(v, 6, B, NH, DH, "bf16", "forward")
     assert pf["algo"] == 1 and pf["ctas_per_group"] == ncl * pf["cluster"], pf
     inp = orc.generate(v, 6, B, NH, DH, seed=21)
+    check_bf16(eng, orc, v, inp)
+
+
+@pytest.mark.parametrize("v,NH,DH,B", [("lstm", 1, 1024, 16), ("slstm", 1, 1024, 20), ("gru", 1, 1152, 16),
+                                       ("slstm", 2, 896, 24)])
+def test_bf16_multicluster_backward(eng, orc, monkeypatch, v, NH, DH, B):
+    """The opt-in multi-cluster backward (FRNN_MC_BWD=1, 4-gate cells): R^T.dg
+    partials for owners in other clusters stored to L2 and pulled by TMA after
+    their sources' release counters, summed after the own cluster's DSMEM
+    partials in a fixed order.  (Shapes not planned by any other test: the
+    plan cache is per shape.)"""
+    monkeypatch.setenv("FRNN_MC_BWD", "1")
+    pb = eng.plan(v, 7, B, NH, DH, "bf16", "backward")
+    assert pb["algo"] == 1 and pb["ctas_per_group"] > pb["cluster"], pb
+    inp = orc.generate(v, 7, B, NH, DH, seed=22)
     check_bf16(eng, orc, v, inp)
 
 
