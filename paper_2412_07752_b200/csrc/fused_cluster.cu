@@ -235,21 +235,6 @@ __device__ __noinline__ void issue_fwd_fixed(uint32_t d1, uint32_t ta, uint32_t 
 }
 
 // ------------------------------------------------------------ forward ----
-// Steps [k0, k1) (16-wide K steps) of a K-split block: steps below nts have A in
-// TMEM (accumulator d1), the rest A in the SMEM M=128 tile (d2), issued
-// interleaved by one uniform PTX loop.  ts / ss: that accumulator already holds
-// a partial sum (updated).
-__device__ __forceinline__ void ksplit_range(uint32_t d1, uint32_t ta, int nts, uint32_t d2, uint64_t a2, uint64_t a2k,
-                                             uint64_t bd, uint64_t bk, uint32_t id, int k0, int k1, int& ts,
-                                             int& ss) {
-  const int ks0 = max(k0, nts);
-  const int n1 = max(0, min(k1, nts) - k0), n2 = max(0, k1 - ks0);
-  mma_chain_ksplit(d1, ta + 8u * k0, bd + (uint64_t)k0 * bk, n1, ts, d2, a2 + (uint64_t)(ks0 - nts) * a2k, a2k,
-                   bd + (uint64_t)ks0 * bk, n2, ss, bk, id);
-  ts |= n1 > 0;
-  ss |= n2 > 0;
-}
-
 // MC = 1: the multi-cluster / K-split instance (NCL > 1 or Ks > 0); MC = 0 keeps
 // the single-cluster code free of those branches (its register allocation and
 // scheduling are what the headline numbers were measured with).
@@ -306,12 +291,30 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, 64)) = v;
     }
   }
-  if (Ks) {  // K columns Kt.. of rows 0..R1-1 -> SMEM, K-major M=128 tile
+  // K-step placement of the split block (MC).  Issue order: the own cluster's
+  // steps [k0, k0+span) first, then the other clusters' steps ("remote", natural
+  // order).  With mclocal each group is split between TMEM and SMEM in the
+  // block's TS:SS ratio, so that both halves overlap their two operand paths:
+  // TMEM positions [0, tsL) = local steps k0.., [tsL, nts) = remote steps 0..;
+  // SMEM positions [0, ssL) = the rest of the local steps, then the rest of the
+  // remote ones.  Without mclocal: TMEM = steps [0, nts), SMEM = [nts, nk).
+  const int nkS = K / 16, ntsS = Kt / 16, nssS = Ks / 16;
+  // (1: two clusters only -- with more, the remote part dominates and arrives piecemeal:
+  //  H=1152 4.03 -> 4.55, H=1408 4.69 -> 5.77 us/step; 2: always)
+  const bool loc = MC && NCL > 1 && (a.mclocal == 2 || (a.mclocal == 1 && NCL == 2));
+  const int spanS = loc ? a.CL * a.UPC / 16 : nkS, k0S = loc ? cl * spanS : 0;
+  const int tsL = loc ? max(max(0, spanS - nssS), min(min(spanS, ntsS), (spanS * ntsS + nkS / 2) / nkS)) : ntsS;
+  const int ssL = spanS - tsL, tsR = ntsS - tsL;
+  auto rstep = [&](int i) { return i < k0S ? i : i + spanS; };
+  auto tpos_k = [&](int j) { return j < tsL ? k0S + j : rstep(j - tsL); };
+  auto spos_k = [&](int j) { return j < ssL ? k0S + tsL + j : rstep(tsR + j - ssL); };
+  if (Ks) {  // the SMEM part of rows 0..R1-1 -> SMEM, K-major M=128 tile (positions: spos_k)
     for (int i = tid; i < 128 * (Ks / 8); i += NT) {
       const int m = i % 128, kc = i / 128, u = m / NGP, g = m % NGP;
+      const int kel = spos_k((kc * 8) >> 4) * 16 + ((kc * 8) & 15);
       uint4 v = make_uint4(0, 0, 0, 0);
       if (m < a.R1 && g < NG && p.rec[g])
-        v = *reinterpret_cast<const uint4*>(R + ((size_t)(hd * NG + g) * DH + unit0 + u) * DH + Kt + kc * 8);
+        v = *reinterpret_cast<const uint4*>(R + ((size_t)(hd * NG + g) * DH + unit0 + u) * DH + kel);
       *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, 128)) = v;
     }
   }
@@ -328,8 +331,9 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int k = 2 * c0 + 8 * q;
+        const int kel = MC ? tpos_k(k >> 4) * 16 + (k & 15) : k;  // (TMEM position k holds K element kel)
         uint4 r4 = make_uint4(0, 0, 0, 0);
-        if (valid && k < DH && k < Kt) r4 = *reinterpret_cast<const uint4*>(src + k);
+        if (valid && k < DH && k < Kt) r4 = *reinterpret_cast<const uint4*>(src + kel);
         v[4 * q] = r4.x;
         v[4 * q + 1] = r4.y;
         v[4 * q + 2] = r4.z;
@@ -404,22 +408,27 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         // (its slices arrive by multicast ~1 k cycles after publishing), then the
         // other clusters' slices once their L2 imports have landed.
         const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 128 * 16, 128), a2k = (2 * 128 * 16) >> 4, bk = (2 * LBO) >> 4;
-        const int nk = K / 16, span = a.CL * a.UPC / 16, k0 = cl * span;
-        int ts = 0, ss = 0;
-        if (NCL > 1 && !a.mclocal) {  // A/B: everything after both barriers, natural K order
-          if (t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
+        const uint32_t d1 = tbase + a.acc1, d2 = tbase + a.acc2;
+        if (!loc) {  // TMEM steps [0, nts), SMEM steps [nts, nk), after every slice arrived
+          if (NCL > 1 && t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
           tc_fence_after();
-          ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, 0, nk, ts, ss);
+          mma_chain_ksplit(d1, tbase, bd, ntsS, 0, d2, a2, a2k, bd + (uint64_t)ntsS * bk, nssS, 0, bk, idesc1);
         } else {
-        ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, k0, k0 + span, ts, ss);
-        if (NCL > 1) {
+          // own cluster's steps: TMEM positions [0, tsL), SMEM positions [0, ssL)
+          mma_chain_ksplit(d1, tbase, bd + (uint64_t)k0S * bk, tsL, 0, d2, a2, a2k, bd + (uint64_t)(k0S + tsL) * bk,
+                           ssL, 0, bk, idesc1);
           if (t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
-          FRNN_PROF(5, t);
           tc_fence_after();
-          ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, 0, k0, ts, ss);
-          ksplit_range(tbase + a.acc1, tbase, Kt / 16, tbase + a.acc2, a2, a2k, bd, bk, idesc1, k0 + span, nk, ts,
-                       ss);
-        }
+          // remote steps r(i) = i (< k0) | i + span, TMEM i in [0, tsR), SMEM i in [tsR, nR): each
+          // stream in two contiguous pieces (before / after the own range)
+          const int nR = nkS - spanS;
+          const int ta_ = min(tsR, k0S), tb_ = tsR - ta_;
+          const int sa_ = max(0, k0S - tsR), sb0 = max(tsR, k0S), sb_ = nR - sb0;
+          mma_chain_ksplit(d1, tbase + 8u * tsL, bd, ta_, tsL > 0, d2, a2 + (uint64_t)ssL * a2k, a2k,
+                           bd + (uint64_t)tsR * bk, sa_, ssL > 0, bk, idesc1);
+          mma_chain_ksplit(d1, tbase + 8u * (tsL + ta_), bd + (uint64_t)(ta_ + spanS) * bk, tb_, tsL + ta_ > 0, d2,
+                           a2 + (uint64_t)(ssL + sa_) * a2k, a2k, bd + (uint64_t)(sb0 + spanS) * bk, sb_,
+                           ssL + sa_ > 0, bk, idesc1);
         }
       } else if (a.R2 && K == 768) {  // H=768 per head: 6 blocks of 8 K-steps, spelled out
         const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 64 * 16, 128);
@@ -1523,8 +1532,9 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   a.mcfence = getenv("FRNN_MC_FENCE") ? atoi(getenv("FRNN_MC_FENCE")) : 0;
   a.mcpoll = getenv("FRNN_MC_POLL") ? atoi(getenv("FRNN_MC_POLL")) : 0;
   a.mcwarp = getenv("FRNN_MC_WARP") ? atoi(getenv("FRNN_MC_WARP")) : 1;
-  // own-cluster K range first: slower while the TMEM/SMEM split is not balanced per range (4.40 vs 4.09 us/step)
-  a.mclocal = getenv("FRNN_MC_LOCAL") ? atoi(getenv("FRNN_MC_LOCAL")) : 0;
+  // own-cluster K steps first, each group split TMEM|SMEM in the block's ratio (H=896 3.59 -> 3.39,
+  // H=1024 3.80 -> 3.68 us/step forward; two clusters only by default)
+  a.mclocal = getenv("FRNN_MC_LOCAL") ? atoi(getenv("FRNN_MC_LOCAL")) : 1;
   a.mcrelw = getenv("FRNN_MC_RELW") ? atoi(getenv("FRNN_MC_RELW")) : 1;
   a.mcdbg = getenv("FRNN_MC_DBG") ? atoi(getenv("FRNN_MC_DBG")) : 0;
   a.p = p;

@@ -335,21 +335,6 @@ __device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t
     mma1_ts_ss(d1, a1 + 8u * k, d2, a2 + (uint64_t)k * a2_step, b0 + (uint64_t)k * b_step, id1, id2,
                k > 0 || acc0);
 }
-// Whole warp.  One block of R rows whose K is split between TMEM (nts steps)
-// and SMEM (nss <= nts steps, M=128 SS form), two accumulators:
-//   D1 (+)= sum_{k<nts} A_tmem(ta + 8k) . B(b0 + k*bk)
-//   D2 (+)= sum_{k<nss} A_smem(a2 + k*a2k) . B(b0 + (nts+k)*bk)
-// issued interleaved so that the TMEM-A and SMEM-A operand paths overlap.
-__device__ __forceinline__ void mma_ksplit(uint32_t d1, uint32_t ta, int nts, uint32_t d2, uint64_t a2, uint64_t a2k,
-                                           int nss, uint64_t b0, uint64_t bk, uint32_t idesc) {
-  const uint64_t b2 = b0 + (uint64_t)nts * bk;
-  int k = 0;
-  for (; k < nss; ++k) {
-    mma1_ts(d1, ta + 8u * k, b0 + (uint64_t)k * bk, idesc, k > 0);
-    mma1_ss(d2, a2 + (uint64_t)k * a2k, b2 + (uint64_t)k * bk, idesc, k > 0);
-  }
-  for (; k < nts; ++k) mma1_ts(d1, ta + 8u * k, b0 + (uint64_t)k * bk, idesc, k > 0);
-}
 // Whole warp, one PTX loop on uniform registers (no per-MMA elect waterfall).
 // Interleaves n1 TMEM-A steps  D1 (+)= A_tmem(ta + 8i) . B(b1 + i*bk)
 // with        n2 SMEM-A steps  D2 (+)= A_smem(a2 + i*a2k) . B(b2 + i*bk);
