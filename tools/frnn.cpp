@@ -3,7 +3,7 @@
 // with a small built-in option parser instead of CLI11.
 //
 //   frnn plan            --variant V --head-dim D --heads H --batch B [--seq T] [--pass forward|backward|both]
-//   frnn feasible-heads  --variant V [--min 16 --max 1024 --step 16 --heads 1 --batch 16]
+//   frnn feasible-heads  --variant V [--min 16 --max 1024 --step 16 --heads 1 --batch 16 --pass both]
 //   frnn solve-csp       <problem.txt>          (text form of include/flashrnn_csp.h)
 //   frnn gradcheck       --variant V [--t 8 --dh 16 --heads 2 --batch 4 --seeds 1 --h 1e-2 --floor 0.1 --tol 1e-2]
 //   frnn precision-drift --variant V [--t 512 --dh 768 --heads 1 --batch 1]
@@ -135,12 +135,16 @@ int cmd_feasible_heads(const Args& a) {
   const frnn_cell c = cell_c(variant_of(a));
   const int lo = (int)a.num("min", 16), hi = (int)a.num("max", 1024), st = (int)a.num("step", 16);
   frnn_options o{0, FRNN_ALGO_FUSED};  // R resident on-chip (the paper's "max fused head dim")
+  const std::string pass = a.str("pass", "both");  // forward | backward | both
+  if (pass != "forward" && pass != "backward" && pass != "both")
+    throw std::invalid_argument("--pass must be forward, backward or both");
   std::ostringstream os;
   for (int dh = lo; dh <= hi; dh += st) {
     const frnn_shape sh{1024, (int32_t)a.num("batch", 16), (int32_t)a.num("heads", 1), dh};
     frnn_plan_info f{}, b{};
-    if (frnn_plan(&c, sh, FRNN_BF16, 0, &o, &f) == FRNN_OK && frnn_plan(&c, sh, FRNN_BF16, 1, &o, &b) == FRNN_OK)
-      os << dh << "\n";
+    const bool fw = pass != "backward" ? frnn_plan(&c, sh, FRNN_BF16, 0, &o, &f) == FRNN_OK : true;
+    const bool bw = pass != "forward" ? frnn_plan(&c, sh, FRNN_BF16, 1, &o, &b) == FRNN_OK : true;
+    if (fw && bw) os << dh << "\n";
   }
   emit(a, os.str());
   return kOk;
