@@ -685,6 +685,26 @@ __device__ __forceinline__ bool issue_bwd_table(int MBT, int MS, int nk, uint32_
   return false;
 }
 
+// The multi-cluster backward's tilings (H = 896 / 1024 / 1152 4-gate), a separate
+// table so that the single-cluster instances keep their code (adding cases to
+// the shared switch moved their register allocation: NH=12 backward +2 %).
+__device__ __forceinline__ bool issue_bwd_table_mc(int MBT, int MS, int nk, uint32_t tbase, uint32_t acc1, uint64_t bd,
+                                                   uint64_t ad, uint32_t idesc, uint32_t idesc2, uint64_t* blkbar) {
+  switch (MBT * 1000 + MS * 100 + nk) {
+#define FRNN_BWD_CASE(M_, S_, K_)                                             \
+  case M_ * 1000 + S_ * 100 + K_:                                             \
+    issue_bwd_fixed<M_, S_, K_>(tbase, acc1, bd, ad, idesc, idesc2, blkbar); \
+    return true;
+    FRNN_BWD_CASE(6, 1, 8) FRNN_BWD_CASE(6, 2, 8) FRNN_BWD_CASE(7, 2, 6)
+#undef FRNN_BWD_CASE
+  }
+  return false;
+}
+
+constexpr bool mc_issue_instance(int MBT, int MS, int nk) {
+  return (MBT == 6 && MS == 1 && nk == 8) || (MBT == 6 && MS == 2 && nk == 8) || (MBT == 7 && MS == 2 && nk == 6);
+}
+
 // ----------------------------------------------------------- backward ----
 // L = 1: the H=768 4-gate layout (every tiling branch fixed at compile time);
 // L = 4: multi-cluster (NCL > 1, 4-gate cells, bf16 column-pair exchange)
@@ -1199,7 +1219,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_bwd_kernel(CArgs a) {
           mma3_ts(acc + 5 * N, tbase + 5 * cb, bd, bk, idesc, 0);
           if (elect_one()) mma_commit(&blkbar[5]);
           __syncwarp();
-        } else if (!FX && N == 16 && SSM == 128 && !a.skeleton && a.itab &&
+        } else if (MCB && N == 16 && SSM == 128 && !a.skeleton && a.itab &&
+                   issue_bwd_table_mc(MBT, MS, nk, tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar)) {
+          // the multi-cluster tilings: compile-time issue (H=1024 backward 8.8 -> 7.6 us/step)
+        } else if (!MCB && !FX && N == 16 && SSM == 128 && !a.skeleton && a.itab &&
                    issue_bwd_table(MBT, MS, nk, tbase, tbase + a.acc1, bd, ad, idesc, idesc2, blkbar)) {
           // every other tiling the planner reaches: compile-time issue instance (scripts/tilings.py)
         } else if (MBT == 2 && MS == 0 && nk == 12 && !a.skeleton) {  // DH=192 per head (config 3)
@@ -1515,6 +1538,7 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
 }
 
 bool cluster_ept_supported(int ept) { return ept == 1; }
+bool cluster_mc_bwd_instance(const ClusterShape& cs) { return mc_issue_instance(cs.MBT, cs.MS, cs.KBP / 16); }
 
 namespace {
 

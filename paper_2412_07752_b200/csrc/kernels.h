@@ -78,6 +78,8 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
 // Clusters of `CL` CTAs of the multi-cluster kernel that can be co-resident (0 without a device).
 int cluster_max_active(const Problem& p, const ClusterShape& cs, bool backward);
 bool cluster_ept_supported(int ept);
+// The multi-cluster backward tiling has a compile-time MMA issue instance (fused_cluster.cu).
+bool cluster_mc_bwd_instance(const ClusterShape& cs);
 cudaError_t cluster_forward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 cudaError_t cluster_backward(const Problem& p, const Plan& pl, void* ws, cudaStream_t s);
 size_t cluster_forward_ws(const Problem& p, const Plan& pl);

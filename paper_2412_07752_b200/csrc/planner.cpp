@@ -256,10 +256,15 @@ bool plan_multicluster(const Problem& p, int pass, const DeviceLimits& lim, Plan
   }
   const int NGP = ngp_of(p.NG), N = 16;
   // Backward (4-gate cells, bf16 column-pair exchange; partials for other clusters'
-  // owners through L2): correct, but measured slower than the alternating backward
-  // (H=1024 LSTM 8.8 vs 8.2 us/step) -- opt-in with FRNN_MC_BWD=1.
-  if (pass == 1 && (NGP != 4 || !getenv("FRNN_MC_BWD") || !atoi(getenv("FRNN_MC_BWD")))) {
-    *why = "multi-cluster backward: opt-in (FRNN_MC_BWD=1), 4-gate cells";
+  // owners through L2): faster than the alternating backward with two clusters on
+  // the tilings with a compile-time MMA issue instance (H=896 7.2-7.3 vs 8.6, H=1024
+  // 7.5-7.6 vs 8.2 us/step); with three clusters box-dependent (H=1152 8.8-9.8 vs
+  // 9.1), with the generic issue loop slower (H=1024 8.8) -- so by default only
+  // two-cluster instance tilings; FRNN_MC_BWD=1 any tiling, =0 none.
+  const char* mcb = getenv("FRNN_MC_BWD");
+  const int mc_bwd = mcb ? atoi(mcb) : -1;
+  if (pass == 1 && (NGP != 4 || mc_bwd == 0)) {
+    *why = "multi-cluster backward: 4-gate cells (FRNN_MC_BWD=0 disables it)";
     return false;
   }
   for (int ncl = 2; ncl <= 9; ++ncl)
@@ -274,6 +279,7 @@ bool plan_multicluster(const Problem& p, int pass, const DeviceLimits& lim, Plan
         continue;
       if (pass == 0 && ((cs.K - cs.Ks) % 16 || cs.Ks % 16)) continue;
       if (pass == 1 && (cs.MBT < 1 || cs.dsm != 2 || !cs.pbf16 || cs.pvec != 2)) continue;
+      if (pass == 1 && mc_bwd < 0 && (ncl > 2 || !cluster_mc_bwd_instance(cs))) continue;
       const int active = cluster_max_active(p, cs, pass == 1);
       if (active > 0 && active < ncl * cs.groups) continue;  // (no device: assume co-resident)
       if (active == 0 && ncl * cs.groups * CL > lim.sm_count) continue;

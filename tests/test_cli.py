@@ -41,7 +41,14 @@ def test_feasible_heads(cli):
     r = cli("feasible-heads", "--variant", "lstm", "--min", 64, "--max", 1024, "--step", 64)
     assert r.returncode == 0
     dims = [int(x) for x in r.stdout.split()]
-    assert 768 in dims and 64 in dims and max(dims) < 1024
+    # one cluster up to 768; beyond, both passes R-resident only on the
+    # multi-cluster tilings with an issue instance (1024: 2 x 16 CTAs)
+    assert 768 in dims and 64 in dims and 1024 in dims
+    r = cli("feasible-heads", "--variant", "lstm", "--min", 1024, "--max", 1536, "--step", 64, "--pass", "forward")
+    assert r.returncode == 0
+    fwd = [int(x) for x in r.stdout.split()]
+    assert 1024 in fwd and 1408 in fwd and 1536 not in fwd
+    assert cli("feasible-heads", "--variant", "lstm", "--pass", "sideways").returncode == 2
 
 
 def test_solve_csp_and_exit_codes(cli, tmp_path):

@@ -208,7 +208,8 @@ def test_bf16_multicluster(eng, orc, v, NH, DH, B, ncl):
     head's units over NCL clusters, h slices of the other clusters imported
     through L2 behind release counters; DH > 960 also splits each CTA's R rows
     along K between TMEM and an SMEM M=128 tile.  B=20: two batch tiles; NH=2:
-    two heads.  Backward: alternating (the default plan)."""
+    two heads.  Backward: multi-cluster for the 4-gate tilings with an issue
+    instance (DH 896/1024/1152), else alternating."""
     pf = eng.plan(v, 6, B, NH, DH, "bf16", "forward")
     assert pf["algo"] == 1 and pf["ctas_per_group"] == ncl * pf["cluster"], pf
     inp = orc.generate(v, 6, B, NH, DH, seed=21)
@@ -218,7 +219,7 @@ def test_bf16_multicluster(eng, orc, v, NH, DH, B, ncl):
 @pytest.mark.parametrize("v,NH,DH,B", [("lstm", 1, 1024, 16), ("slstm", 1, 1024, 20), ("gru", 1, 1152, 16),
                                        ("slstm", 2, 896, 24)])
 def test_bf16_multicluster_backward(eng, orc, monkeypatch, v, NH, DH, B):
-    """The opt-in multi-cluster backward (FRNN_MC_BWD=1, 4-gate cells): R^T.dg
+    """The multi-cluster backward (FRNN_MC_BWD=1: for any tiling): R^T.dg
     partials for owners in other clusters stored to L2 and pulled by TMA after
     their sources' release counters, summed after the own cluster's DSMEM
     partials in a fixed order.  (Shapes not planned by any other test: the
