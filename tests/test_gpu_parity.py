@@ -231,6 +231,18 @@ def test_bf16_multicluster_backward(eng, orc, monkeypatch, v, NH, DH, B):
     check_bf16(eng, orc, v, inp)
 
 
+@pytest.mark.parametrize("v,clip,mag", [("slstm", "value", 0.05), ("lstm", "zero", 0.0), ("gru", "off", 0.0)])
+def test_bf16_multicluster_clip_ragged_step_grads(eng, orc, v, clip, mag):
+    """Multi-cluster forward + backward (H=1024, two clusters) with gradient
+    clipping (the remote partials are summed before the clip), a ragged second
+    batch tile (B=21) and per-step hidden gradients."""
+    T, B, DH = 8, 21, 1024
+    assert eng.plan(v, T, B, 1, DH, "bf16", "backward")["ctas_per_group"] == 32
+    inp = orc.generate(v, T, B, 1, DH, seed=23)
+    dh = 0.5 * np.random.RandomState(3).randn(T, B, DH)
+    check_bf16(eng, orc, v, inp, clip, mag, dh=dh)
+
+
 @pytest.mark.parametrize("NH,DH", [(1, 768), (1, 512), (2, 96)])
 def test_bf16_gru_compact_k(eng, orc, monkeypatch, NH, DH):
     """GRU backward with the n gate's (zero) R rows dropped from the R^T.dg K
