@@ -1,3 +1,7 @@
+"""Per-step stamps of the multi-cluster forward (frnn_debug_profile): local / remote h arrival, MMA halves, publish.
+
+    python scripts/mc_profile.py 1024
+"""
 import ctypes as C, os, statistics as S, sys
 sys.path.insert(0, os.getcwd())
 import torch
