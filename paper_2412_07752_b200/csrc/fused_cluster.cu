@@ -1639,13 +1639,17 @@ cudaError_t cluster_launch(KernelT kern, const CArgs& a, int grid, int threads, 
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = a.CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  // Multi-cluster kernels spin on each other's counters: a cooperative launch
+  // guarantees every cluster is resident (or fails) instead of trapping later
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.NCL > 1 ? 2 : 1;
   note_launch();
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
