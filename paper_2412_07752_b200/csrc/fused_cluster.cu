@@ -93,6 +93,7 @@ struct CArgs {
                    //        0 = [n/2][cu] layout, N/2 4-byte pushes per lane
   int NCL;         // forward: clusters per group; > 1: slices of other clusters imported through L2
   int Ks;          // forward: K columns of the R rows in SMEM (M=128 SS, second accumulator)
+  int m64;         // forward (MC): rows <= 64 -- TMEM half M=128 (lanes 64.. zero), SMEM half an M=64 tile
   uint32_t* xflags;  // forward, NCL > 1: [groups][NCL*CL] step counters of the published slices
   int mcfence, mcpoll;  // NCL > 1: full fence before the flag release; relaxed polling (A/B knobs)
   int mcwarp, mclocal;  // NCL > 1: the importing warp; own cluster's K range issued first (A/B knobs)
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   uint8_t* hB0 = smem;                       // [N x K] K-major (step parity 0)
   uint8_t* hB1 = hB0 + N * K * 2;            // (step parity 1)
   uint8_t* A2 = hB1 + N * K * 2;             // [64 x K] K-major, rows R1..R1+R2 (or [128 x Ks]: K split)
-  float* xs = reinterpret_cast<float*>(A2 + (a.R2 ? 64 * K * 2 : 128 * Ks * 2));  // [N][ROWS+1]
+  float* xs = reinterpret_cast<float*>(A2 + (a.R2 ? 64 * K * 2 : (MC && a.m64 ? 64 : 128) * Ks * 2));  // [N][ROWS+1]
   uint8_t* hs = reinterpret_cast<uint8_t*>(xs + N * XP);               // my h slice
   uint64_t* bars = reinterpret_cast<uint64_t*>(hs + ((a.slice + 15) & ~15u));  // mma, x0, x1
   // bars: MMA done, h(t) parity 0/1 (own cluster's slices), MC: other clusters' slices parity 0/1
@@ -308,14 +309,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
   auto rstep = [&](int i) { return i < k0S ? i : i + spanS; };
   auto tpos_k = [&](int j) { return j < tsL ? k0S + j : rstep(j - tsL); };
   auto spos_k = [&](int j) { return j < ssL ? k0S + tsL + j : rstep(tsR + j - ssL); };
-  if (Ks) {  // the SMEM part of rows 0..R1-1 -> SMEM, K-major M=128 tile (positions: spos_k)
-    for (int i = tid; i < 128 * (Ks / 8); i += NT) {
-      const int m = i % 128, kc = i / 128, u = m / NGP, g = m % NGP;
+  const bool m64 = MC && a.m64;
+  const int MR = m64 ? 64 : 128;  // rows of the split block's MMAs
+  if (Ks) {  // the SMEM part of rows 0..R1-1 -> SMEM, K-major M=MR tile (positions: spos_k)
+    for (int i = tid; i < MR * (Ks / 8); i += NT) {
+      const int m = i % MR, kc = i / MR, u = m / NGP, g = m % NGP;
       const int kel = spos_k((kc * 8) >> 4) * 16 + ((kc * 8) & 15);
       uint4 v = make_uint4(0, 0, 0, 0);
       if (m < a.R1 && g < NG && p.rec[g])
         v = *reinterpret_cast<const uint4*>(R + ((size_t)(hd * NG + g) * DH + unit0 + u) * DH + kel);
-      *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, 128)) = v;
+      *reinterpret_cast<uint4*>(A2 + kmaj(m, kc * 8, MR)) = v;
     }
   }
   tc_fence_before();
@@ -407,16 +410,18 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         // One M=128 block, K split TMEM | SMEM.  The own cluster's K range first
         // (its slices arrive by multicast ~1 k cycles after publishing), then the
         // other clusters' slices once their L2 imports have landed.
-        const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 128 * 16, 128), a2k = (2 * 128 * 16) >> 4, bk = (2 * LBO) >> 4;
+        const uint64_t a2 = sdesc_kmajor(smem_u32(A2), MR * 16, 128), a2k = (uint64_t)(2 * MR * 16) >> 4,
+                       bk = (2 * LBO) >> 4;
         const uint32_t d1 = tbase + a.acc1, d2 = tbase + a.acc2;
+        const uint32_t ids = m64 ? idesc2 : idesc1;  // the SMEM half: M=64 tile for blocks of <= 64 rows
         if (!loc) {  // TMEM steps [0, nts), SMEM steps [nts, nk), after every slice arrived
           if (NCL > 1 && t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
           tc_fence_after();
-          mma_chain_ksplit(d1, tbase, bd, ntsS, 0, d2, a2, a2k, bd + (uint64_t)ntsS * bk, nssS, 0, bk, idesc1);
+          mma_chain_ksplit(d1, tbase, bd, ntsS, 0, d2, a2, a2k, bd + (uint64_t)ntsS * bk, nssS, 0, bk, idesc1, ids);
         } else {
           // own cluster's steps: TMEM positions [0, tsL), SMEM positions [0, ssL)
           mma_chain_ksplit(d1, tbase, bd + (uint64_t)k0S * bk, tsL, 0, d2, a2, a2k, bd + (uint64_t)(k0S + tsL) * bk,
-                           ssL, 0, bk, idesc1);
+                           ssL, 0, bk, idesc1, ids);
           if (t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
           tc_fence_after();
           // remote steps r(i) = i (< k0) | i + span, TMEM i in [0, tsR), SMEM i in [tsR, nR): each
@@ -425,10 +430,10 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
           const int ta_ = min(tsR, k0S), tb_ = tsR - ta_;
           const int sa_ = max(0, k0S - tsR), sb0 = max(tsR, k0S), sb_ = nR - sb0;
           mma_chain_ksplit(d1, tbase + 8u * tsL, bd, ta_, tsL > 0, d2, a2 + (uint64_t)ssL * a2k, a2k,
-                           bd + (uint64_t)tsR * bk, sa_, ssL > 0, bk, idesc1);
+                           bd + (uint64_t)tsR * bk, sa_, ssL > 0, bk, idesc1, ids);
           mma_chain_ksplit(d1, tbase + 8u * (tsL + ta_), bd + (uint64_t)(ta_ + spanS) * bk, tb_, tsL + ta_ > 0, d2,
                            a2 + (uint64_t)(ssL + sa_) * a2k, a2k, bd + (uint64_t)(sb0 + spanS) * bk, sb_,
-                           ssL + sa_ > 0, bk, idesc1);
+                           ssL + sa_ > 0, bk, idesc1, ids);
         }
       } else if (a.R2 && K == 768) {  // H=768 per head: 6 blocks of 8 K-steps, spelled out
         const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 64 * 16, 128);
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
     if (w < 4) {
       float v[16];
       tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc1, v);
-      if (Ks) {
+      if (Ks && !m64) {  // (m64: accumulator 2 is an M=64 tile, added below)
         float v2[16];
         tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc2, v2);
 #pragma unroll
@@ -502,6 +507,17 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       if (32 * w + l < a.R1) {
 #pragma unroll
         for (int n = 0; n < N; ++n) xs[n * XP + xs_row(32 * w + l)] = v[n];
+      }
+    }
+    if (m64) {
+      __syncthreads();
+      if (w < 4) {
+        float v2[16];
+        tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + a.acc2, v2);
+        if (l < 16 && 16 * w + l < a.R1) {
+#pragma unroll
+          for (int n = 0; n < N; ++n) xs[n * XP + xs_row(16 * w + l)] += v2[n];
+        }
       }
     } else if (w < 8 && a.R2) {  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
       const int q = w & 3;
@@ -1472,7 +1488,8 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
     s.acc1 = (uint32_t)align_up((s.K - s.Ks) / 2, 32);
     s.acc2 = s.acc1 + N;
     s.tmem_cols = pow2_cols(s.acc2 + N);
-    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : (size_t)128 * s.Ks * 2) +
+    s.m64 = s.NCL > 1 && rows <= 64 && !getenv("FRNN_FWD_NOM64");
+    s.smem = (size_t)2 * N * s.K * 2 + (s.R2 ? (size_t)64 * s.K * 2 : (size_t)(s.m64 ? 64 : 128) * s.Ks * 2) +
              (size_t)N * xs_pitch(rows) * 4 + align_up(s.slice, 16) + 64;
     // (x and the trace move by per-thread loads/stores: TMA tiles measured slower)
     s.ws = align_up((size_t)s.groups * 2 * s.NCL * s.CL * s.slice, 256);
@@ -1551,6 +1568,7 @@ CArgs make_cargs(const Problem& p, const Plan& pl, void* ws, bool backward, Clus
   CArgs a{};
   a.NCL = cs.NCL;
   a.Ks = cs.Ks;
+  a.m64 = backward ? 0 : cs.m64;
   // (the slice writers' stores reach the flag's release through bar.sync; a full
   // fence before it measured 0.47 us/step slower at H=1024 and is not needed)
   a.mcfence = getenv("FRNN_MC_FENCE") ? atoi(getenv("FRNN_MC_FENCE")) : 0;

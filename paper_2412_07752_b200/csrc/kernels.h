@@ -71,6 +71,7 @@ struct ClusterShape {
   size_t smem, ws;
   int NCL;  // clusters per group (> 1: h slices / partials cross clusters through L2 with release counters)
   int Ks;   // forward: K columns of the R rows held in SMEM (M=128 SS) when K/2 + accumulators exceed TMEM
+  int m64;  // forward, multi-cluster: rows <= 64 -- both halves of the K split as M=64 MMAs
 };
 // ncl > 1: the group's DH units are split over ncl clusters of
 // DH / (UPC * ncl) CTAs each.

@@ -338,10 +338,10 @@ __device__ __forceinline__ void mma_run_ts_ss(uint32_t d1, uint32_t a1, uint32_t
 // Whole warp, one PTX loop on uniform registers (no per-MMA elect waterfall).
 // Interleaves n1 TMEM-A steps  D1 (+)= A_tmem(ta + 8i) . B(b1 + i*bk)
 // with        n2 SMEM-A steps  D2 (+)= A_smem(a2 + i*a2k) . B(b2 + i*bk);
-// accumulate = (i > 0) || acc1 (resp. acc2).
+// accumulate = (i > 0) || acc1 (resp. acc2); idesc for the TMEM-A, idesc_s for the SMEM-A MMAs.
 __device__ __forceinline__ void mma_chain_ksplit(uint32_t d1, uint32_t ta, uint64_t b1, int n1, uint32_t acc1,
                                                  uint32_t d2, uint64_t a2, uint64_t a2k, uint64_t b2, int n2,
-                                                 uint32_t acc2, uint64_t bk, uint32_t idesc) {
+                                                 uint32_t acc2, uint64_t bk, uint32_t idesc, uint32_t idesc_s) {
   asm volatile(
       "{\n\t.reg .pred e, q, r, s, g, h, p1, p2, z1, z2;\n\t.reg .b32 k, ta, n;\n\t.reg .b64 bb1, aa2, bb2;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -352,12 +352,12 @@ __device__ __forceinline__ void mma_chain_ksplit(uint32_t d1, uint32_t ta, uint6
       "setp.lt.s32 r, k, %3;\n\tsetp.lt.s32 s, k, %9;\n\tand.pred g, e, r;\n\tand.pred h, e, s;\n\t"
       "setp.ne.or.b32 p1, k, 0, z1;\n\tsetp.ne.or.b32 p2, k, 0, z2;\n\t"
       "@g tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bb1, %12, p1;\n\t"
-      "@h tcgen05.mma.cta_group::1.kind::f16 [%5], aa2, bb2, %12, p2;\n\t"
+      "@h tcgen05.mma.cta_group::1.kind::f16 [%5], aa2, bb2, %13, p2;\n\t"
       "add.u32 ta, ta, 8;\n\tadd.u64 bb1, bb1, %11;\n\tadd.u64 aa2, aa2, %7;\n\tadd.u64 bb2, bb2, %11;\n\t"
       "add.s32 k, k, 1;\n\tsetp.lt.s32 q, k, n;\n\t@q bra.uni KS_LOOP%=;\n\t"
       "KS_END%=:\n\t}" ::"r"(d1),
       "r"(ta), "l"(b1), "r"(n1), "r"(acc1), "r"(d2), "l"(a2), "l"(a2k), "l"(b2), "r"(n2), "r"(acc2), "l"(bk),
-      "r"(idesc)
+      "r"(idesc), "r"(idesc_s)
       : "memory");
 }
 // 12-step blocks: a whole K=192 backward block (UPC=48, 4-gate cells) per asm.

@@ -44,10 +44,10 @@ def test_feasible_heads(cli):
     # one cluster up to 768; beyond, both passes R-resident only on the
     # multi-cluster tilings with an issue instance (1024: 2 x 16 CTAs)
     assert 768 in dims and 64 in dims and 1024 in dims
-    r = cli("feasible-heads", "--variant", "lstm", "--min", 1024, "--max", 1536, "--step", 64, "--pass", "forward")
+    r = cli("feasible-heads", "--variant", "lstm", "--min", 1024, "--max", 2048, "--step", 64, "--pass", "forward")
     assert r.returncode == 0
     fwd = [int(x) for x in r.stdout.split()]
-    assert 1024 in fwd and 1408 in fwd and 1536 not in fwd
+    assert 1024 in fwd and 1408 in fwd and 1536 in fwd and 2048 not in fwd
     assert cli("feasible-heads", "--variant", "lstm", "--pass", "sideways").returncode == 2
 
 

@@ -202,7 +202,8 @@ def test_bf16_other_head_dims(eng, orc, v, NH, DH, B):
 
 @pytest.mark.parametrize("v,NH,DH,B,ncl", [("lstm", 1, 1024, 16, 2), ("slstm", 1, 1024, 20, 2),
                                            ("gru", 1, 1152, 16, 3), ("elman", 1, 1024, 8, 2),
-                                           ("slstm", 2, 896, 16, 2), ("lstm", 1, 1408, 16, 4)])
+                                           ("slstm", 2, 896, 16, 2), ("lstm", 1, 1408, 16, 4),
+                                           ("gru", 1, 1536, 16, 6)])
 def test_bf16_multicluster(eng, orc, v, NH, DH, B, ncl):
     """R-resident forward beyond one cluster (fused_cluster.cu, NCL > 1): the
     head's units over NCL clusters, h slices of the other clusters imported
