@@ -508,8 +508,16 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
 #pragma unroll
         for (int n = 0; n < N; ++n) xs[n * XP + xs_row(32 * w + l)] = v[n];
       }
+    } else if (w < 8 && a.R2) {  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
+      const int q = w & 3;
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + a.acc2, v);
+      if (l < 16 && 16 * q + l < a.R2) {
+#pragma unroll
+        for (int n = 0; n < N; ++n) xs[n * XP + xs_row(a.R1 + 16 * q + l)] = v[n];
+      }
     }
-    if (m64) {
+    if (m64) {  // the split block's M=64 SMEM half, added to the drained M=128 half
       __syncthreads();
       if (w < 4) {
         float v2[16];
@@ -518,14 +526,6 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
 #pragma unroll
           for (int n = 0; n < N; ++n) xs[n * XP + xs_row(16 * w + l)] += v2[n];
         }
-      }
-    } else if (w < 8 && a.R2) {  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
-      const int q = w & 3;
-      float v[16];
-      tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + a.acc2, v);
-      if (l < 16 && 16 * q + l < a.R2) {
-#pragma unroll
-        for (int n = 0; n < N; ++n) xs[n * XP + xs_row(a.R1 + 16 * q + l)] = v[n];
       }
     }
     tc_fence_before();
