@@ -136,6 +136,13 @@ FRNN_API int frnn_workspace_size(const frnn_cell* cell, frnn_shape shape, int32_
  * planner.cpp:428-453): shape, kernel family, tiling, footprint, solve time. */
 FRNN_API int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
                             const frnn_options* opts, char* out, size_t out_bytes);
+/* Re-check of the solved plan against every constraint of its kernel family
+ * (the counterpart of rnnkit::plan::plan_residuals, planner.cpp:349-402): writes
+ * a JSON array of violations ("[]" when every residual is zero) and returns
+ * FRNN_OK, or FRNN_EINFEASIBLE when there is any.  frnn_plan_json also reports
+ * the plan's per-step traffic (hbm_traffic_per_step, planner.cpp:233-243). */
+FRNN_API int frnn_plan_check(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                             const frnn_options* opts, char* out, size_t out_bytes);
 /* Persistent plan cache (the paper's cached solver solutions):
  * JSON lines, one solved plan per line (schema_version 1), tagged with the
  * library version and device limits; load skips lines from another build or

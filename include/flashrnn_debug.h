@@ -35,6 +35,15 @@ FRNN_API int frnn_debug_plan_csp(const frnn_cell* cell, frnn_shape shape, int32_
  * UPC, CL, MBT, MS, SSM, KBP, R1, R2} (zeros past `cluster` when not clustered). */
 FRNN_API int frnn_debug_cluster_shape(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
                                       int32_t* out10);
+/* The internal plan of a pass as 16 fields {algo, rows_per_cta, batch_tile,
+ * units_per_cta, ctas_per_group, groups, grid, threads, smem_bytes, tmem_cols,
+ * k_split, cluster, ka, stages, ffma, workspace_bytes}, and the residual check
+ * (frnn_plan_check) of an arbitrary such plan -- tests corrupt a field and
+ * expect a violation. */
+FRNN_API int frnn_debug_plan_fields(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                                    const frnn_options* opts, int64_t* fields16);
+FRNN_API int frnn_debug_plan_residuals(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                                       const int64_t* fields16, char* out, size_t out_bytes);
 /* The placement half of frnn_dist_gather (flashrnn_dist.h) for a `world`-rank
  * layout, from a caller-filled staging buffer [world][blk] (what ncclAllGather
  * would deliver) into the full tensor k (0 states, 1 gates, 2 dx, 3 ds0, 4 dR,

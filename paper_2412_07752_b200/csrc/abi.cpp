@@ -394,7 +394,9 @@ int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32
   if ((rc = get_plan(p, pass, opts, &pl))) return rc;
   static const char* algos[] = {"auto", "fused", "alternating", "simt"};
   const auto& lim = frnn::device_limits();
-  char buf[2048];
+  const frnn::PlanTraffic tr = frnn::plan_traffic(p, pass, pl);
+  const std::vector<std::string> res = frnn::plan_residuals(p, pass, pl, lim);
+  char buf[2560];
   const int n = std::snprintf(
       buf, sizeof buf,
       "{\n  \"schema_version\": 1,\n  \"gpu\": \"B200\",\n  \"sm_count\": %d,\n  \"pass\": \"%s\",\n"
@@ -406,15 +408,98 @@ int frnn_plan_json(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32
       "\"step_kernels\": \"%s\"},\n"
       "  \"grid_blocks\": %d,\n  \"threads_per_block\": %d,\n"
       "  \"footprint\": {\"smem_bytes\": %d, \"tmem_columns\": %d, \"workspace_bytes\": %lld, "
-      "\"r_matrix_bytes_per_head\": %lld},\n  \"solve_us\": %.1f\n}\n",
+      "\"r_matrix_bytes_per_head\": %lld},\n"
+      "  \"traffic_per_step_bytes\": {\"io\": %.0f, \"exchange_onchip\": %.0f, \"exchange_l2\": %.0f, "
+      "\"r_stream\": %.0f},\n  \"residuals\": %d,\n  \"solve_us\": %.1f\n}\n",
       lim.sm_count, pass == FRNN_PASS_FORWARD ? "forward" : "backward", p.NS, p.NG, p.DH, p.NH, p.B, p.T,
       p.bf16 ? "bf16" : "fp32", algos[pl.algo & 3], pl.cluster, pl.units_per_cta, pl.rows_per_cta, pl.batch_tile,
       pl.ctas_per_group, pl.groups, pl.k_split, pl.ka, pl.stages,
       pl.algo == FRNN_ALGO_SIMT ? "simt" : (pl.ffma || !p.bf16) ? "ffma" : "tcgen05", pl.grid, pl.threads, pl.smem_bytes, pl.tmem_cols,
-      (long long)pl.ws_bytes, (long long)p.NG * p.DH * p.DH * (p.bf16 ? 2 : 4), pl.solve_us);
+      (long long)pl.ws_bytes, (long long)p.NG * p.DH * p.DH * (p.bf16 ? 2 : 4), tr.io, tr.exchange_onchip,
+      tr.exchange_l2, tr.r_stream, (int)res.size(), pl.solve_us);
   if (!out || n < 0 || (size_t)n + 1 > out_bytes) return fail(FRNN_EINVAL_ARG, "output buffer too small");
   std::memcpy(out, buf, (size_t)n + 1);
   return FRNN_OK;
+}
+
+namespace {
+std::string json_escape(const std::string& m) {
+  std::string o;
+  for (char c : m) {
+    if (c == '"' || c == '\\') o += '\\';
+    o += c;
+  }
+  return o;
+}
+int write_residuals(const std::vector<std::string>& res, char* out, size_t out_bytes) {
+  std::string j = "[";
+  for (size_t i = 0; i < res.size(); ++i) j += (i ? ", \"" : "\"") + json_escape(res[i]) + "\"";
+  j += "]";
+  if (!out || j.size() + 1 > out_bytes) return fail(FRNN_EINVAL_ARG, "output buffer too small");
+  std::memcpy(out, j.c_str(), j.size() + 1);
+  return res.empty() ? FRNN_OK : fail(FRNN_EINFEASIBLE, "plan residuals: " + res[0]);
+}
+frnn::Plan plan_from_fields(const int64_t* f) {
+  frnn::Plan pl{};
+  pl.algo = (int)f[0];
+  pl.rows_per_cta = (int)f[1];
+  pl.batch_tile = (int)f[2];
+  pl.units_per_cta = (int)f[3];
+  pl.ctas_per_group = (int)f[4];
+  pl.groups = (int)f[5];
+  pl.grid = (int)f[6];
+  pl.threads = (int)f[7];
+  pl.smem_bytes = (int)f[8];
+  pl.tmem_cols = (int)f[9];
+  pl.k_split = (int)f[10];
+  pl.cluster = (int)f[11];
+  pl.ka = (int)f[12];
+  pl.stages = (int)f[13];
+  pl.ffma = (int)f[14];
+  pl.ws_bytes = (size_t)f[15];
+  return pl;
+}
+}  // namespace
+
+int frnn_plan_check(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass, const frnn_options* opts,
+                    char* out, size_t out_bytes) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, pass, opts, &pl))) return rc;
+  return write_residuals(frnn::plan_residuals(p, pass, pl, frnn::device_limits()), out, out_bytes);
+}
+
+int frnn_debug_plan_fields(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                           const frnn_options* opts, int64_t* fields16) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
+  if (!fields16) return fail(FRNN_EINVAL_ARG, "null output");
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  frnn::Plan pl{};
+  if ((rc = get_plan(p, pass, opts, &pl))) return rc;
+  const int64_t f[16] = {pl.algo, pl.rows_per_cta, pl.batch_tile, pl.units_per_cta, pl.ctas_per_group, pl.groups,
+                         pl.grid, pl.threads, pl.smem_bytes, pl.tmem_cols, pl.k_split, pl.cluster, pl.ka, pl.stages,
+                         pl.ffma, (int64_t)pl.ws_bytes};
+  std::memcpy(fields16, f, sizeof f);
+  return FRNN_OK;
+}
+
+int frnn_debug_plan_residuals(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,
+                              const int64_t* fields16, char* out, size_t out_bytes) {
+  g_err.clear();
+  int rc = validate(cell, shape, dtype);
+  if (rc) return rc;
+  if ((rc = validate_pass(pass))) return rc;
+  if (!fields16) return fail(FRNN_EINVAL_ARG, "null plan");
+  frnn::Problem p = make_problem(cell, shape, dtype);
+  return write_residuals(frnn::plan_residuals(p, pass, plan_from_fields(fields16), frnn::device_limits()), out,
+                         out_bytes);
 }
 
 int frnn_workspace_size(const frnn_cell* cell, frnn_shape shape, int32_t dtype, int32_t pass,

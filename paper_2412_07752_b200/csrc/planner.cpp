@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -447,6 +448,119 @@ size_t plan_workspace(const Problem& p, int pass, const Plan& pl) {
       if (pl.ffma) return pass == 0 ? alt32_forward_ws(p) : alt32_backward_ws(p);
       return pass == 0 ? alt_forward_ws(p, pl) : alt_backward_ws(p, pl);
   }
+}
+
+std::vector<std::string> plan_residuals(const Problem& p, int pass, const Plan& pl, const DeviceLimits& lim) {
+  std::vector<std::string> out;
+  auto fail = [&out](const std::string& m) { out.push_back(m); };
+  auto eq = [&](long long a, long long b, const char* what) {
+    if (a != b) fail(std::string(what) + ": plan " + std::to_string(a) + ", recomputed " + std::to_string(b));
+  };
+  const bool bwd = pass == 1;
+  const int NGP = ngp_of(p.NG), N = pl.batch_tile;
+  if (pl.threads < 32 || pl.threads % 32 || pl.threads > lim.max_threads) fail("threads not a warp multiple within the block limit");
+  if (pl.smem_bytes > lim.smem_optin) fail("shared memory exceeds the opt-in limit");
+  if (pl.tmem_cols > lim.tmem_cols) fail("TMEM columns exceed the SM's 512");
+  if (pl.tmem_cols && (pl.tmem_cols < 32 || (pl.tmem_cols & (pl.tmem_cols - 1)))) fail("TMEM allocation not a power of two >= 32");
+  if (pl.grid != pl.groups * pl.ctas_per_group) fail("grid != groups x CTAs per group");
+  eq((long long)pl.ws_bytes, (long long)plan_workspace(p, pass, pl), "workspace bytes");
+  if (pl.algo == FRNN_ALGO_FUSED && pl.cluster > 0) {  // cluster-resident (one or several clusters)
+    const int CL = pl.cluster, UPC = pl.units_per_cta;
+    if (pl.ctas_per_group % CL) {
+      fail("CTAs per group not a multiple of the cluster");
+      return out;
+    }
+    const int ncl = pl.ctas_per_group / CL;
+    if (CL > lim.cluster_max) fail("cluster larger than the device's non-portable maximum");
+    if ((long long)UPC * pl.ctas_per_group != p.DH) fail("units per CTA x CTAs per group != head dim");
+    eq(pl.rows_per_cta, UPC * NGP, "rows per CTA");
+    eq(pl.groups, p.NH * ((p.B + N - 1) / N), "groups (heads x batch tiles)");
+    if (UPC % 2 || UPC / 2 * N > 384) fail("one unit pair per thread needs UPC even and UPC/2 x N <= 384");
+    const ClusterShape cs = cluster_shape(p, UPC, N, bwd, ncl);
+    eq(pl.smem_bytes, (long long)cs.smem, "shared memory");
+    eq(pl.tmem_cols, cs.tmem_cols, "TMEM columns");
+    eq(pl.threads, cs.threads, "threads");
+    if (!cluster_ept_supported(cs.EPT)) fail("element ownership unsupported");
+    if (!bwd) {
+      if (ncl == 1 && (cs.R1 > 128 || cs.R2 > 64)) fail("rows exceed the TMEM (128) + SMEM (64) blocks");
+      if (ncl > 1 && (cs.R2 != 0 || UPC % 8 || (CL * UPC) % 16)) fail("multi-cluster slice geometry");
+      if ((cs.K - cs.Ks) % 16 || cs.Ks % 16) fail("K split not in whole 16-wide steps");
+    } else {
+      if (cs.MBT < 1) fail("no R^T column block in TMEM");
+      if (std::max(cs.MBT, cs.MS) > 16) fail("more than 16 block pairs");
+      if (ncl > 1 && (NGP != 4 || cs.dsm != 2 || !cs.pbf16 || cs.pvec != 2)) fail("multi-cluster backward exchange");
+    }
+    const int active = cluster_max_active(p, cs, bwd && ncl > 1);
+    if (ncl > 1 && active > 0 && active < ncl * pl.groups) fail("clusters of a group not co-resident");
+    if (ncl > 1 && active == 0 && pl.grid > lim.sm_count) fail("grid exceeds the SM count");
+    int regs = 0, local = 0, maxt = 0;
+    if (ncl == 1 && cluster_kernel_attrs(p.variant, bwd, &regs, &local, &maxt) &&
+        (long long)regs * pl.threads > lim.regs_per_sm)
+      fail("registers x threads exceed the register file");
+  } else if (pl.algo == FRNN_ALGO_FUSED) {  // L2-flag fused kernels
+    if ((long long)pl.units_per_cta * pl.ctas_per_group != p.DH) fail("units per CTA x CTAs per group != head dim");
+    eq(pl.tmem_cols, fused_tmem_cols(p, N, bwd), "TMEM columns");
+    if (pl.grid > lim.sm_count) fail("cooperative grid exceeds the SM count");
+  } else if (pl.algo == FRNN_ALGO_ALTERNATING && !pl.ffma) {
+    std::string why;
+    if (!alt_supported(p, &why)) fail(why);
+    const AltShape sh = alt_shape(p, bwd, N, pl.k_split, pl.ka, pl.stages);
+    eq(pl.smem_bytes, (long long)sh.smem, "shared memory");
+    eq(pl.tmem_cols, sh.tmem_cols, "TMEM columns");
+    eq(pl.grid, sh.grid, "grid");
+    if ((size_t)sh.stages * sh.stage_bytes > sh.region) fail("stage ring exceeds its region");
+    if ((long long)sh.ka * sh.kpg * 64 != p.DH) fail("K atoms x atoms per gate != head dim");
+    if (p.B > N * sh.NBT) fail("batch tiles do not cover the batch");
+  } else if (pl.algo == FRNN_ALGO_SIMT) {
+    eq(pl.smem_bytes, (long long)simt_smem_bytes(p, bwd), "shared memory");
+  }
+  return out;
+}
+
+PlanTraffic plan_traffic(const Problem& p, int pass, const Plan& pl) {
+  PlanTraffic t{};
+  const double e = p.bf16 ? 2 : 4, B = p.B, D = p.D, NS = p.NS, NG = p.NG, DH = p.DH, NH = p.NH;
+  int nin = 0, nrec = 0;
+  for (int j = 0; j < p.NG; ++j) {
+    nin += p.inp[j];
+    nrec += p.rec[j];
+  }
+  const bool alt = pl.algo == FRNN_ALGO_ALTERNATING;
+  const double N = pl.batch_tile > 0 ? pl.batch_tile : 16, nbt = std::ceil(B / N);
+  if (pass == 0) {  // engine.hpp:170-201: x_t in, gates_t and states_{t+1} out
+    t.io = B * nin * D * e + B * NG * D * e + B * NS * D * e;
+    if (alt) t.io += 2 * NS * B * D * 4;  // fp32 carry in and out
+    const double h = B * D * e;           // the h_t all-gather source
+    if (pl.algo == FRNN_ALGO_FUSED && pl.cluster > 0) {
+      const int ncl = std::max(1, pl.ctas_per_group / pl.cluster);
+      t.exchange_l2 = h + h * (ncl - 1) / ncl;  // slices staged in L2, the other clusters' slices imported
+      t.exchange_onchip = h * pl.cluster;       // multicast delivery into every CTA of a cluster
+    } else if (pl.algo == FRNN_ALGO_FUSED) {
+      t.exchange_l2 = h + h * pl.ctas_per_group;  // every CTA of a group re-reads all of h
+    } else if (alt) {
+      const double tiles = std::ceil(DH * (p.NG == 1 ? 1.0 : 4.0) / 128.0);
+      t.exchange_l2 = h * tiles;                  // every unit tile streams h
+      t.r_stream = nrec * DH * DH * NH * e;
+    }
+  } else {  // engine.hpp:257-336: the trace in, dh in, dx out
+    t.io = B * (NS + NG) * D * e + B * NG * D * e;
+    if (alt) t.io += 2 * NS * B * D * 4;
+    const double part = B * D * 4;  // one fp32 R^T.dg partial per CTA source and column
+    if (pl.algo == FRNN_ALGO_FUSED && pl.cluster > 0) {
+      const int ncl = std::max(1, pl.ctas_per_group / pl.cluster);
+      const double pb = p.NG == 4 ? 2 : 4;  // bf16-pair partials for 4-gate cells
+      t.exchange_onchip = B * D * pb * pl.cluster;                     // every source pushes every column
+      t.exchange_l2 = ncl > 1 ? B * D * pb * pl.cluster * (ncl - 1) : 0;  // columns owned by other clusters
+    } else if (pl.algo == FRNN_ALGO_FUSED) {
+      t.exchange_l2 = 2 * part * pl.ctas_per_group;
+    } else if (alt) {
+      t.exchange_onchip = part * pl.k_split;  // split-K partials through DSMEM
+      t.exchange_l2 = B * nrec * D * e * std::ceil(DH / 128.0);  // dg streamed by every column tile
+      t.r_stream = nrec * DH * DH * NH * e;
+    }
+    (void)nbt;
+  }
+  return t;
 }
 
 std::string plan_csp_text(const Problem& p, int pass, int algo, const DeviceLimits& lim) {
