@@ -361,18 +361,23 @@ bool plan_fused(const Problem& p, int pass, const DeviceLimits& lim, Plan* out, 
     *why = "fused: shared memory";
     return false;
   }
-  int best = 0;
-  for (int upc = 128 / NGP; upc >= 1; --upc)
-    if (p.DH % upc == 0) {
-      best = upc;
-      break;
-    }
-  const int CPG = p.DH / best;
-  const int grid = p.NH * NBT * CPG;
-  if (grid > lim.sm_count) {
-    *why = "fused: grid of " + std::to_string(grid) + " CTAs exceeds co-residency";
+  // The L2-flag kernels' tiling CSP: UPC units per CTA (all NGP gates of each:
+  // at most one 128-lane TMEM block of rows), CPG CTAs per group with
+  // UPC x CPG = DH, every group's CTAs co-resident (cooperative launch);
+  // heuristic: fewest CTAs synchronising per step (largest UPC).
+  Builder b;
+  auto vU = b.var("UPC", Domain::span(1, std::max(1, 128 / NGP)));
+  auto vC = b.var("CPG", Domain::span(1, std::max(1, p.DH)));
+  b.eq(vU * vC, p.DH);
+  b.le(vC * (p.NH * NBT), lim.sm_count);
+  b.prefer("UPC", Pref::Largest);
+  const auto sol = run(b);
+  if (!sol) {
+    *why = "fused: no UPC x CPG split of the head with the grid co-resident";
     return false;
   }
+  const int best = (int)sol->at("UPC"), CPG = (int)sol->at("CPG");
+  const int grid = p.NH * NBT * CPG;
   Plan& pl = *out;
   pl = Plan{};
   pl.algo = FRNN_ALGO_FUSED;
