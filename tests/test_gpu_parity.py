@@ -244,6 +244,28 @@ def test_bf16_multicluster_clip_ragged_step_grads(eng, orc, v, clip, mag):
     check_bf16(eng, orc, v, inp, clip, mag, dh=dh)
 
 
+@pytest.mark.parametrize("T", [0, 1, 2])
+def test_multicluster_short_sequences(eng, orc, T):
+    """Multi-cluster kernels (H=1024, two clusters per pass) at T = 0 / 1 / 2:
+    no step, a single step (no h exchange at all), one exchange."""
+    inp = orc.generate("lstm", T, 16, 1, 1024, seed=41)
+    assert eng.plan("lstm", T, 16, 1, 1024, "bf16", "forward")["ctas_per_group"] == 32
+    gpu = run_gpu(eng, "lstm", inp, True)
+    ora = run_oracle(orc, "lstm", inp, True)
+    keys = ("states", "dbias", "dR", "ds0") + (("gates", "dx") if T else ())
+    assert_close(gpu, ora, BF16_TOL, keys)
+
+
+def test_multicluster_falls_back_when_not_coresident(eng, orc):
+    """B=256 at H=1024 needs 16 batch tiles x 2 clusters of 16 CTAs: more
+    clusters than can be resident at once, so the planner must not pick the
+    multi-cluster kernels (they spin on each other); the fallback is correct."""
+    pf = eng.plan("lstm", 2, 256, 1, 1024, "bf16", "forward")
+    assert not (pf["algo"] == 1 and pf["ctas_per_group"] > pf["cluster"] > 0), pf
+    inp = orc.generate("lstm", 2, 256, 1, 1024, seed=42)
+    check_bf16(eng, orc, "lstm", inp)
+
+
 @pytest.mark.parametrize("NH,DH", [(1, 768), (1, 512), (2, 96)])
 def test_bf16_gru_compact_k(eng, orc, monkeypatch, NH, DH):
     """GRU backward with the n gate's (zero) R rows dropped from the R^T.dg K
