@@ -35,7 +35,19 @@
 // bf16x2.  MMAs are issued by warp 0 as straight-line PTX blocks (sm100.cuh
 // mma8_* / mma12_*, issue_bwd_fixed for every tiling the planner reaches).
 // Backward instances: L = 0 generic (all A/B switches), 1 the H=768 4-gate
-// layout, 2 / 3 lean (default exchange only; 3 also without split coefficients).
+// layout, 2 / 3 lean (default exchange only; 3 also without split coefficients),
+// 4 multi-cluster.
+//
+// Multi-cluster (NCL > 1, heads beyond one cluster; forward instance MC = 1,
+// backward L = 4): the group's units over NCL clusters.  Forward: each CTA's
+// block of <= 128 rows is split along K between TMEM and an SMEM tile (M=128,
+// or M=64 for blocks of <= 64 rows) with two accumulators; the own cluster's h
+// slices arrive by the multicast above, the other clusters' slices are imported
+// through L2 (per-slice step counters released by each writer CTA, polled by
+// lanes of warp 1, TMA multicast into the own cluster).  Backward: partials for
+// owners in the own cluster by DSMEM as above, for other clusters' owners stored
+// to L2 and pulled by TMA after the source's release counter.  Launched as
+// cooperative cluster grids (every cluster resident or the launch fails).
 #include <cuda_bf16.h>
 
 #include <algorithm>
