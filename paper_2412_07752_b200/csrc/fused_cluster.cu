@@ -417,8 +417,7 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
       FRNN_PROF(1, t);
       tc_fence_after();
       const uint64_t bd = sdesc_kmajor(smem_u32(buf ? hB1 : hB0), LBO, SBO);
-      if (a.skeleton) {
-      } else if (MC) {
+      if (MC) {  // (skeleton mode: the barrier waits still run, only the MMAs are skipped)
         // One M=128 block, K split TMEM | SMEM.  The own cluster's K range first
         // (its slices arrive by multicast ~1 k cycles after publishing), then the
         // other clusters' slices once their L2 imports have landed.
@@ -429,11 +428,13 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
         if (!loc) {  // TMEM steps [0, nts), SMEM steps [nts, nk), after every slice arrived
           if (NCL > 1 && t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
           tc_fence_after();
-          mma_chain_ksplit(d1, tbase, bd, ntsS, 0, d2, a2, a2k, bd + (uint64_t)ntsS * bk, nssS, 0, bk, idesc1, ids);
+          if (!a.skeleton)
+            mma_chain_ksplit(d1, tbase, bd, ntsS, 0, d2, a2, a2k, bd + (uint64_t)ntsS * bk, nssS, 0, bk, idesc1, ids);
         } else {
           // own cluster's steps: TMEM positions [0, tsL), SMEM positions [0, ssL)
-          mma_chain_ksplit(d1, tbase, bd + (uint64_t)k0S * bk, tsL, 0, d2, a2, a2k, bd + (uint64_t)(k0S + tsL) * bk,
-                           ssL, 0, bk, idesc1, ids);
+          if (!a.skeleton)
+            mma_chain_ksplit(d1, tbase, bd + (uint64_t)k0S * bk, tsL, 0, d2, a2, a2k, bd + (uint64_t)(k0S + tsL) * bk,
+                             ssL, 0, bk, idesc1, ids);
           if (t > 0) mbar_wait_cluster(&bars[3 + buf], ((t - 1) >> 1) & 1);
           tc_fence_after();
           // remote steps r(i) = i (< k0) | i + span, TMEM i in [0, tsR), SMEM i in [tsR, nR): each
@@ -441,12 +442,15 @@ __global__ void __launch_bounds__(MAXT, 1) cl_fwd_kernel(CArgs a) {
           const int nR = nkS - spanS;
           const int ta_ = min(tsR, k0S), tb_ = tsR - ta_;
           const int sa_ = max(0, k0S - tsR), sb0 = max(tsR, k0S), sb_ = nR - sb0;
-          mma_chain_ksplit(d1, tbase + 8u * tsL, bd, ta_, tsL > 0, d2, a2 + (uint64_t)ssL * a2k, a2k,
-                           bd + (uint64_t)tsR * bk, sa_, ssL > 0, bk, idesc1, ids);
-          mma_chain_ksplit(d1, tbase + 8u * (tsL + ta_), bd + (uint64_t)(ta_ + spanS) * bk, tb_, tsL + ta_ > 0, d2,
-                           a2 + (uint64_t)(ssL + sa_) * a2k, a2k, bd + (uint64_t)(sb0 + spanS) * bk, sb_,
-                           ssL + sa_ > 0, bk, idesc1, ids);
+          if (!a.skeleton) {
+            mma_chain_ksplit(d1, tbase + 8u * tsL, bd, ta_, tsL > 0, d2, a2 + (uint64_t)ssL * a2k, a2k,
+                             bd + (uint64_t)tsR * bk, sa_, ssL > 0, bk, idesc1, ids);
+            mma_chain_ksplit(d1, tbase + 8u * (tsL + ta_), bd + (uint64_t)(ta_ + spanS) * bk, tb_, tsL + ta_ > 0, d2,
+                             a2 + (uint64_t)(ssL + sa_) * a2k, a2k, bd + (uint64_t)(sb0 + spanS) * bk, sb_,
+                             ssL + sa_ > 0, bk, idesc1, ids);
+          }
         }
+      } else if (a.skeleton) {
       } else if (a.R2 && K == 768) {  // H=768 per head: 6 blocks of 8 K-steps, spelled out
         const uint64_t a2 = sdesc_kmajor(smem_u32(A2), 64 * 16, 128);
         constexpr uint64_t a2k = (2 * 64 * 16) >> 4, bk = (2 * LBO) >> 4;
