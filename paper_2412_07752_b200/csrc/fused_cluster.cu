@@ -1498,7 +1498,7 @@ ClusterShape cluster_shape(const Problem& p, int UPC, int N, bool backward, int 
       int nts = (nk * 90 + 139) / 140;
       const char* kt = getenv("FRNN_FWD_KT");  // A/B hook: TMEM K columns of the split
       if (kt) nts = atoi(kt) / 16;
-      nts = std::max(nk / 2, std::min(nts, (512 - 2 * N) / 8));
+      nts = std::min(std::max(nk / 2, nts), (512 - 2 * N) / 8);  // (the TMEM cap wins)
       s.Ks = s.K - 16 * nts;
     }
     s.acc1 = (uint32_t)align_up((s.K - s.Ks) / 2, 32);
