@@ -218,7 +218,7 @@ def test_bf16_multicluster(eng, orc, v, NH, DH, B, ncl):
 
 
 @pytest.mark.parametrize("v,NH,DH,B", [("lstm", 1, 1024, 16), ("slstm", 1, 1024, 20), ("gru", 1, 1152, 16),
-                                       ("slstm", 2, 896, 24)])
+                                       ("slstm", 2, 896, 24), ("lstm", 1, 960, 16), ("gru", 1, 832, 8)])
 def test_bf16_multicluster_backward(eng, orc, monkeypatch, v, NH, DH, B):
     """The multi-cluster backward (FRNN_MC_BWD=1: for any tiling): R^T.dg
     partials for owners in other clusters stored to L2 and pulled by TMA after
